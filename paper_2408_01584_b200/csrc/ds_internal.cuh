@@ -1,0 +1,40 @@
+// ds_internal.cuh -- handle layout and kernel launchers shared by the .cu files.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "../../include/drivesim_b200.h"
+#include "ds_math.cuh"
+
+struct ds_handle {
+  ds_tables tab;
+  ds_config cfg;
+  ds_state st;
+  int device;
+  int num_sms;
+  int obs_width;
+  int step_threads;     // threads per world CTA in the step kernel
+  size_t step_smem;     // dynamic shared memory of the step kernel
+  int obs_warps;        // warps per world CTA in the observation kernel
+  size_t obs_smem;
+  uint32_t ring_read;   // host mirror of entries already drained
+};
+
+namespace ds {
+
+// Sizes of the per-warp selection scratch in the radial observation kernel.
+constexpr int kCandCap = 384;   // candidates kept before a streaming compaction
+constexpr int kSelCap = 128;    // bucket-threshold survivors sorted exactly
+constexpr int kBuckets = 256;   // first-level distance histogram
+
+cudaError_t launch_step(const ds_handle *h, const ds_step_args *a, cudaStream_t s);
+cudaError_t launch_reset(const ds_handle *h, const uint8_t *mask, float *rewards,
+                         uint8_t *dones, cudaStream_t s);
+cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, float *obs,
+                           const float *inv_scale, int32_t *sel_idx, cudaStream_t s);
+size_t obs_smem_bytes(const ds_config &cfg, int max_agents, int warps, int obs_width);
+size_t step_smem_bytes(int max_agents);
+cudaError_t configure_kernels(int max_dynamic_smem);
+cudaError_t configure_step_kernels(int max_dynamic_smem);
+
+}  // namespace ds

@@ -1,0 +1,402 @@
+// ds_step.cu -- the fused per-world step kernel and the reset kernel.
+//
+// One CTA per world, one thread per agent (blockDim = A_max rounded up to a
+// warp).  A world is share-nothing (engine.py:4-7), so a CTA owns it for the
+// whole step and the four phases of World.step (engine.py:357-498) are
+// separated by __syncthreads only:
+//   A  dynamics of live controlled agents + expert replay   (engine.py:378-418)
+//   B  SAT agent-agent and slab agent-road-edge collisions   (engine.py:420-459)
+//   C  goal reward, removal, collision behaviour, horizon    (engine.py:461-492)
+//   D  outputs, episode record, optional VecDriveEnv auto-reset
+// State is FP64 in HBM (SURVEY.md §7 "hard parts"); the broad phase is exact
+// brute force over the world's agents held in shared memory and over the road
+// edges binned in the world's uniform grid (the reference's BVH only prunes:
+// its results are pinned equal to brute force, tests/test_acceptance.py:193-219).
+#include "ds_internal.cuh"
+
+namespace ds {
+
+struct StepShared {
+  double *x, *y, *c, *s, *hl, *hw;
+  uint8_t *elig;
+};
+
+__device__ __forceinline__ StepShared carve_step(void *base, int amax) {
+  StepShared sh;
+  double *d = reinterpret_cast<double *>(base);
+  sh.x = d;
+  sh.y = d + amax;
+  sh.c = d + 2 * amax;
+  sh.s = d + 3 * amax;
+  sh.hl = d + 4 * amax;
+  sh.hw = d + 5 * amax;
+  sh.elig = reinterpret_cast<uint8_t *>(d + 6 * amax);
+  return sh;
+}
+
+size_t step_smem_bytes(int max_agents) {
+  return (size_t)max_agents * (6 * sizeof(double) + 1) + 16;
+}
+
+// SAT over the 4 box axes, _fastpath.sat_pairs (fp:29-53); (i, j) with i < j.
+__device__ __forceinline__ bool sat_hit(const StepShared &sh, int i, int j) {
+  const double dx = sh.x[j] - sh.x[i];
+  const double dy = sh.y[j] - sh.y[i];
+  const double ci = sh.c[i], si = sh.s[i], cj = sh.c[j], sj = sh.s[j];
+  const double hli = sh.hl[i], hwi = sh.hw[i], hlj = sh.hl[j], hwj = sh.hw[j];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    double ax, ay;
+    if (m == 0) { ax = ci; ay = si; }
+    else if (m == 1) { ax = -si; ay = ci; }
+    else if (m == 2) { ax = cj; ay = sj; }
+    else { ax = -sj; ay = cj; }
+    const double dist = fabs(dx * ax + dy * ay);
+    const double ra = hli * fabs(ci * ax + si * ay) + hwi * fabs(ci * ay - si * ax);
+    const double rb = hlj * fabs(cj * ax + sj * ay) + hwj * fabs(cj * ay - sj * ax);
+    if (dist > ra + rb) return false;
+  }
+  return true;
+}
+
+// Segment vs oriented box slab clip in the box frame, _fastpath.seg_box_hits
+// (fp:55-90); boundary contact counts as a hit.
+__device__ __forceinline__ bool seg_box_hit(double cx, double cy, double ck, double sk,
+                                            double hl, double hw, double sax, double say,
+                                            double sbx, double sby) {
+  const double rax = sax - cx, ray = say - cy, rbx = sbx - cx, rby = sby - cy;
+  const double pax = rax * ck + ray * sk;
+  const double pay = -rax * sk + ray * ck;
+  const double pbx = rbx * ck + rby * sk;
+  const double pby = -rbx * sk + rby * ck;
+  double t0 = 0.0, t1 = 1.0;
+#pragma unroll
+  for (int axis = 0; axis < 2; ++axis) {
+    const double p0 = axis == 0 ? pax : pay;
+    const double d = axis == 0 ? (pbx - pax) : (pby - pay);
+    const double h = axis == 0 ? hl : hw;
+    if (d == 0.0) {
+      if (p0 < -h || p0 > h) return false;
+    } else {
+      double ta = (-h - p0) / d;
+      double tb = (h - p0) / d;
+      if (ta > tb) { const double tmp = ta; ta = tb; tb = tmp; }
+      if (ta > t0) t0 = ta;
+      if (tb < t1) t1 = tb;
+      if (t0 > t1) return false;
+    }
+  }
+  return true;
+}
+
+// Clamp a floating cell coordinate to [lo, hi] before converting.
+__device__ __forceinline__ int cell_of(double v, int lo, int hi) {
+  double f = floor(v);
+  if (f < (double)lo) return lo;
+  if (f > (double)hi) return hi;
+  return (int)f;
+}
+
+// Any road-edge segment of world w touching box (cx, cy, ck, sk, hl, hw)?
+__device__ bool offroad_query(const ds_tables &T, const ds_config &C, int w, double cx,
+                              double cy, double ck, double sk, double hl, double hw) {
+  const int nx = T.grid_nx[w], ny = T.grid_ny[w];
+  const double x0 = T.grid_x0[w], y0 = T.grid_y0[w], cs = C.grid_cell;
+  const int64_t cbase = T.grid_cell_off[w];
+  // AABB of the box (agent_aabbs_core fp:304-317) with 1.1 cm slack: the grid
+  // only has to produce a superset, the slab test below decides.
+  const double rx = hl * fabs(ck) + hw * fabs(sk) + 0.011;
+  const double ry = hl * fabs(sk) + hw * fabs(ck) + 0.011;
+  const double gx0 = (cx - rx - x0) / cs, gx1 = (cx + rx - x0) / cs;
+  const double gy0 = (cy - ry - y0) / cs, gy1 = (cy + ry - y0) / cs;
+  if (gx1 < 0.0 || gy1 < 0.0 || gx0 >= (double)nx || gy0 >= (double)ny) return false;
+  const int ix0 = cell_of(gx0, 0, nx - 1), ix1 = cell_of(gx1, 0, nx - 1);
+  const int iy0 = cell_of(gy0, 0, ny - 1), iy1 = cell_of(gy1, 0, ny - 1);
+  for (int iy = iy0; iy <= iy1; ++iy) {
+    for (int ix = ix0; ix <= ix1; ++ix) {
+      const int64_t cell = cbase + (int64_t)iy * nx + ix;
+      const int b = T.eseg_cell_start[cell], e = T.eseg_cell_start[cell + 1];
+      for (int k = b; k < e; ++k) {
+        if (seg_box_hit(cx, cy, ck, sk, hl, hw, T.eseg_ax[k], T.eseg_ay[k], T.eseg_bx[k],
+                        T.eseg_by[k]))
+          return true;
+      }
+    }
+  }
+  return false;
+}
+
+// Reset one agent of world w to t = 0 (World.reset, engine.py:318-340).
+__device__ __forceinline__ void reset_agent(const ds_tables &T, const ds_state &S, int64_t g,
+                                            int64_t r0) {
+  S.x[g] = T.rep_x[r0];
+  S.y[g] = T.rep_y[r0];
+  S.heading[g] = T.rep_h[r0];
+  S.speed[g] = T.rep_v[r0];
+  S.head_angle[g] = 0.0;
+  const bool present = T.rep_present[r0] || (T.sflags[g] & DS_SF_CONTROLLED);
+  S.flags[g] = present ? DS_F_PRESENT : 0;
+}
+
+__global__ void __launch_bounds__(1024) step_kernel(ds_tables T, ds_config C, ds_state S,
+                                                    ds_step_args a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int w = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int64_t a0 = T.a_off[w];
+  const int A = (int)(T.a_off[w + 1] - a0);
+  const int64_t r_w = T.r_off[w];
+  const int Tw = T.num_steps[w];
+  const bool act_here = tid < A;
+  const int64_t g = a0 + tid;
+  const uint8_t sf = act_here ? T.sflags[g] : 0;
+  const bool ctrl = sf & DS_SF_CONTROLLED;
+  const int row = (act_here && ctrl) ? T.ctrl_row[g] : -1;
+  const int n_rows = (int)(T.c_off[w + 1] - T.c_off[w]);
+
+  if (S.episode_over[w]) {
+    // Early return of World.step (engine.py:370-373): zero rewards/info,
+    // dones = done[ids]; observation rows are all done -> zero.
+    if (row >= 0) {
+      a.rewards[row] = 0.0f;
+      a.dones[row] = (S.flags[g] & DS_F_DONE) ? 1 : 0;
+      a.info[row] = 0;
+      a.info[T.n_rows + row] = 0;
+      a.info[2 * T.n_rows + row] = 0;
+    }
+    if (a.auto_reset) {
+      if (act_here) reset_agent(T, S, g, r_w + tid);
+      if (row >= 0) a.rewards[row] = 0.0f;
+      if (tid == 0) {
+        S.t[w] = 0;
+        S.episode_over[w] = 0;
+      }
+    }
+    return;
+  }
+
+  StepShared sh = carve_step(smem_raw, T.max_agents);
+  const int t = S.t[w];
+  const int t_next = min(t + 1, Tw - 1);
+  const double dt = T.dt[w];
+  const int64_t rn = r_w + (int64_t)t_next * A + tid;   // replay cell at t_next
+
+  uint16_t f = 0;
+  double x = 0, y = 0, h = 0, v = 0;
+  if (act_here) {
+    f = S.flags[g];
+    // (1) remove agents flagged last step (engine.py:379-380)
+    if (f & DS_F_PENDING) f |= DS_F_REMOVED;
+    f &= ~(DS_F_PENDING | DS_F_COLLIDED | DS_F_OFFROAD);
+    x = S.x[g];
+    y = S.y[g];
+    h = S.heading[g];
+    v = S.speed[g];
+    const bool live = ctrl && !(f & (DS_F_REMOVED | DS_F_DONE));
+    if (!a.replay && live) {
+      // Action row (engine.py:392: float64 cast of the caller's values).
+      double a0v = 0.0, a1v = 0.0, a2v = 0.0, a3v = 0.0;
+      if (a.actions) {
+        const float *ar = a.actions + (int64_t)row * a.act_dim;
+        a0v = ar[0];
+        a1v = ar[1];
+        if (a.act_dim > 2) a2v = ar[2];
+        if (a.act_dim > 3) a3v = ar[3];
+      } else {
+        // VecDriveEnv.to_continuous (env.py:111-116): divmod by n_steer.
+        int idx = a.action_idx[row];
+        int ai = idx >= 0 ? idx / a.n_steer : -((-idx + a.n_steer - 1) / a.n_steer);
+        int si = idx - ai * a.n_steer;
+        if (ai < 0) ai += a.n_accel;
+        ai = min(max(ai, 0), a.n_accel - 1);
+        a0v = a.grid_accel[ai];
+        a1v = a.grid_steer[si];
+      }
+      const double L = T.length[g];
+      if (C.dynamics == DS_DYN_CLASSIC) {
+        // classic_core (fp:319-333), left-to-right, no FMA.
+        const double acc = clip(a0v, C.accel_lo, C.accel_hi);
+        const double delta = clip(a1v, C.steer_lo, C.steer_hi);
+        const double v_bar = clip(v + 0.5 * acc * dt, -C.v_max, C.v_max);
+        const double tdelta = tan(delta);
+        const double beta = atan(0.5 * tdelta);
+        const double ang = h + beta;
+        x += v_bar * cos(ang) * dt;
+        y += v_bar * sin(ang) * dt;
+        h = wrap(h + v_bar * cos(beta) * tdelta / L * dt);
+        v = clip(v + acc * dt, -C.v_max, C.v_max);
+      } else if (C.dynamics == DS_DYN_INVERTIBLE) {
+        // invertible_core (fp:335-342); actions are not clipped.
+        const double d = v * dt + 0.5 * a0v * dt * dt;
+        x += d * cos(h);
+        y += d * sin(h);
+        h = wrap(h + a1v * d);
+        v = clip(v + a0v * dt, -C.v_max, C.v_max);
+      } else {
+        // delta_local: ego-frame displacement (dx, dy) and yaw
+        // increment, clipped to SimConfig.delta_bounds; speed = |d| / dt.
+        const double ddx = clip(a0v, C.delta_lo[0], C.delta_hi[0]);
+        const double ddy = clip(a1v, C.delta_lo[1], C.delta_hi[1]);
+        const double dyaw = clip(a2v, C.delta_lo[2], C.delta_hi[2]);
+        const double ch = cos(h), shh = sin(h);
+        x += ddx * ch - ddy * shh;
+        y += ddx * shh + ddy * ch;
+        h = wrap(h + dyaw);
+        v = clip(hypot(ddx, ddy) / dt, -C.v_max, C.v_max);
+      }
+      // Head rotation (engine.py:408-411), column 2 (column 3 for delta_local).
+      const int head_col = C.dynamics == DS_DYN_DELTA_LOCAL ? 3 : 2;
+      if (a.actions && a.act_dim > head_col) {
+        const double hr = head_col == 2 ? a2v : a3v;
+        S.head_angle[g] = clip(S.head_angle[g] + hr * dt, -0.5 * kPi, 0.5 * kPi);
+      }
+    }
+    // Expert replay (engine.py:383-385, 413-418).
+    const bool replay_i = (sf & DS_SF_REPLAY_ONLY) || (a.replay && ctrl);
+    if (replay_i && (sf & DS_SF_INSTANTIABLE) && !(f & DS_F_REMOVED)) {
+      x = T.rep_x[rn];
+      y = T.rep_y[rn];
+      h = T.rep_h[rn];
+      v = T.rep_v[rn];
+      if (T.rep_present[rn]) f |= DS_F_PRESENT; else f &= ~DS_F_PRESENT;
+    }
+    S.x[g] = x;
+    S.y[g] = y;
+    S.heading[g] = h;
+    S.speed[g] = v;
+    // (2-3) collision inputs (engine.py:424-428)
+    sh.x[tid] = x;
+    sh.y[tid] = y;
+    sh.c[tid] = cos(h);
+    sh.s[tid] = sin(h);
+    sh.hl[tid] = T.half_l[g];
+    sh.hw[tid] = T.half_w[g];
+    const bool elig = (f & DS_F_PRESENT) && !(f & DS_F_REMOVED) &&
+                      ((ctrl && !(f & DS_F_DONE)) || T.rep_valid[rn]);
+    sh.elig[tid] = elig;
+  }
+  __syncthreads();
+
+  bool collided = false, offroad = false;
+  if (act_here && sh.elig[tid]) {
+    for (int j = 0; j < A; ++j) {
+      if (j == tid || !sh.elig[j]) continue;
+      if (j > tid ? sat_hit(sh, tid, j) : sat_hit(sh, j, tid)) {
+        collided = true;
+        break;
+      }
+    }
+    if (!(sf & DS_SF_PEDESTRIAN))
+      offroad = offroad_query(T, C, w, sh.x[tid], sh.y[tid], sh.c[tid], sh.s[tid], sh.hl[tid],
+                              sh.hw[tid]);
+  }
+  if (collided) f |= DS_F_COLLIDED;
+  if (offroad) f |= DS_F_OFFROAD;
+
+  // (4) goal rewards, then terminations (engine.py:461-486).
+  bool at_goal = false, live = false;
+  if (n_rows > 0 && act_here) {
+    live = ctrl && !(f & (DS_F_REMOVED | DS_F_DONE));
+    if (live) {
+      const double dgx = x - T.goal_x[g];
+      const double dgy = y - T.goal_y[g];
+      at_goal = hypot(dgx, dgy) <= C.goal_tolerance;
+    }
+    if (at_goal) f |= DS_F_GOAL_REACHED | DS_F_GOAL_EVER | DS_F_PENDING | DS_F_DONE;
+    if (collided && live) f |= DS_F_COLL_EVER;
+    if (offroad && live) f |= DS_F_OFF_EVER;
+    if (C.collision_behavior == DS_COLL_REMOVE_AGENT && live && (collided || offroad))
+      f |= DS_F_PENDING | DS_F_DONE;
+  }
+  const int any_end = __syncthreads_or(C.collision_behavior == DS_COLL_END_EPISODE && live &&
+                                        (collided || offroad));
+  bool over = any_end != 0;
+  const int t1 = t + 1;
+  if (t1 >= Tw) over = true;
+  if (over && ctrl) f |= DS_F_DONE;
+
+  if (row >= 0) {
+    a.rewards[row] = at_goal ? 1.0f : 0.0f;
+    a.dones[row] = (f & DS_F_DONE) ? 1 : 0;
+    a.info[row] = at_goal;
+    a.info[T.n_rows + row] = collided && live;
+    a.info[2 * T.n_rows + row] = offroad && live;
+  }
+  if (act_here) S.flags[g] = f;
+
+  if (over) {
+    // EpisodeInfo at the episode's end (engine.py:521-528, 646-647).
+    const int n_goal = __syncthreads_count(ctrl && (f & DS_F_GOAL_EVER));
+    const int n_coll = __syncthreads_count(ctrl && (f & DS_F_COLL_EVER));
+    const int n_off = __syncthreads_count(ctrl && (f & DS_F_OFF_EVER));
+    if (tid == 0 && S.ring) {
+      const uint32_t pos = atomicAdd(S.ring_head, 1u);
+      if (pos < (uint32_t)S.ring_cap) {
+        int32_t *rec = S.ring + (int64_t)pos * 6;
+        rec[0] = a.serial;
+        rec[1] = w;
+        rec[2] = n_rows;
+        rec[3] = n_goal;
+        rec[4] = n_coll;
+        rec[5] = n_off;
+      }
+    }
+    if (a.auto_reset) {
+      // VecDriveEnv.step auto-reset (env.py:105-107): World.reset of the
+      // finished world; SimBatch.reset zeroes the rewards buffer rows the env
+      // returns (engine.py:660), dones/infos were copied before.
+      __syncthreads();
+      if (act_here) reset_agent(T, S, g, r_w + tid);
+      if (row >= 0) a.rewards[row] = 0.0f;
+      if (tid == 0) {
+        S.t[w] = 0;
+        S.episode_over[w] = 0;
+      }
+      return;
+    }
+  }
+  if (tid == 0) {
+    S.t[w] = t1;
+    S.episode_over[w] = over ? 1 : 0;
+  }
+}
+
+__global__ void __launch_bounds__(1024) reset_kernel(ds_tables T, ds_state S, const uint8_t *mask,
+                                                     float *rewards, uint8_t *dones) {
+  const int w = blockIdx.x;
+  if (mask && !mask[w]) return;
+  const int64_t a0 = T.a_off[w];
+  const int A = (int)(T.a_off[w + 1] - a0);
+  for (int i = threadIdx.x; i < A; i += blockDim.x) {
+    const int64_t g = a0 + i;
+    reset_agent(T, S, g, T.r_off[w] + i);
+    if (T.sflags[g] & DS_SF_CONTROLLED) {
+      const int row = T.ctrl_row[g];
+      if (rewards) rewards[row] = 0.0f;
+      if (dones) dones[row] = 0;
+    }
+  }
+  if (threadIdx.x == 0) {
+    S.t[w] = 0;
+    S.episode_over[w] = 0;
+  }
+}
+
+cudaError_t configure_step_kernels(int max_dynamic_smem) {
+  return cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              max_dynamic_smem);
+}
+
+cudaError_t launch_step(const ds_handle *h, const ds_step_args *a, cudaStream_t s) {
+  step_kernel<<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg, h->st, *a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reset(const ds_handle *h, const uint8_t *mask, float *rewards, uint8_t *dones,
+                         cudaStream_t s) {
+  int threads = h->step_threads;
+  reset_kernel<<<h->tab.n_worlds, threads, 0, s>>>(h->tab, h->st, mask, rewards, dones);
+  return cudaGetLastError();
+}
+
+}  // namespace ds

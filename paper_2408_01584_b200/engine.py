@@ -1,0 +1,526 @@
+"""Batched multi-world simulation on one B200: the drop-in for the reference's
+``SimBatch`` (pkg/src/drivesim/engine.py:582-677).
+
+Every world's state lives in HBM as structure-of-arrays FP64 (packing.py);
+``step`` enqueues two kernels on the caller's CUDA stream (the fused world step
+and the observation kernel, csrc/) through the C ABI and returns the SAME torch
+buffers every call, exactly like the reference returns its reused numpy
+buffers (engine.py:648-649).  There is no host synchronisation inside
+``step``/``reset``; the only synchronising calls are the explicit readbacks
+(``episode_infos``, ``episode_over_host``, ``worlds``).
+
+Documented deviations from the reference surface:
+  * observations / rewards are float32 tensors on the device (the reference
+    emits float64 numpy); dones / info are torch.bool;
+  * actions are consumed as float32 (the oracle sees the same values upcast);
+  * ``n_workers`` is accepted and ignored (the GPU replaces the fork pool; one
+    process per GPU owns a world shard, see ``parallel.py``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .config import ObsConfig, SimConfig, obs_width
+from .device_layout import DeviceLayout, build_layout
+from .packing import PackedWorlds, RawWorlds, pack, raw_from_prepared
+
+
+class ActionCountMismatch(ValueError):
+    pass
+
+
+class NoControllableAgents(UserWarning):
+    pass
+
+
+@dataclass
+class EpisodeInfo:
+    scenario: str
+    world_id: int
+    n_controlled: int
+    n_goal: int
+    n_veh_collision: int
+    n_offroad: int
+
+
+@dataclass
+class Metrics:
+    goal_rate: float
+    veh_collision_rate: float
+    offroad_rate: float
+    episodes: int
+
+
+@dataclass
+class StepOutput:
+    observations: torch.Tensor  # (n_controlled_total, obs_width) f32, device
+    rewards: torch.Tensor       # (n_controlled_total,) f32
+    dones: torch.Tensor         # (n_controlled_total,) bool
+    info: dict                  # goal / veh_collision / offroad bool tensors
+
+
+@dataclass
+class ThroughputReport:
+    worlds: int
+    steps: int
+    elapsed_s: float
+    total_agents: int
+    controlled_agents: int
+    asps: float = 0.0
+    casps: float = 0.0
+
+    def __post_init__(self):
+        # engine.py:146-148
+        self.asps = self.steps * self.total_agents / self.elapsed_s
+        self.casps = self.steps * self.controlled_agents / self.elapsed_s
+
+
+def compute_metrics(episode_infos: list) -> Metrics:
+    """engine.py:151-163."""
+    if not episode_infos:
+        raise ValueError("no completed episodes")
+    total = sum(e.n_controlled for e in episode_infos)
+    if total == 0:
+        return Metrics(0.0, 0.0, 0.0, len(episode_infos))
+    return Metrics(goal_rate=sum(e.n_goal for e in episode_infos) / total,
+                   veh_collision_rate=sum(e.n_veh_collision for e in episode_infos) / total,
+                   offroad_rate=sum(e.n_offroad for e in episode_infos) / total,
+                   episodes=len(episode_infos))
+
+
+METRICS_CSV_HEADER = "scenario,episode,controlled,goal_rate,veh_collision_rate,offroad_rate"
+BENCH_CSV_HEADER = "worlds,steps,total_agents,controlled_agents,elapsed_s,asps,casps"
+
+
+def metrics_csv_row(e: EpisodeInfo, episode: int) -> str:
+    n = max(e.n_controlled, 1)
+    return (f"{e.scenario},{episode},{e.n_controlled},"
+            f"{e.n_goal / n},{e.n_veh_collision / n},{e.n_offroad / n}")
+
+
+def bench_csv_row(r: ThroughputReport) -> str:
+    return (f"{r.worlds},{r.steps},{r.total_agents},{r.controlled_agents},"
+            f"{r.elapsed_s},{r.asps},{r.casps}")
+
+
+def make_native_config(cfg: SimConfig, grid_cell: float) -> N.DsConfig:
+    o = cfg.obs
+    c = N.DsConfig()
+    c.dynamics = N.DYN[cfg.dynamics]
+    c.collision_behavior = N.COLL[cfg.collision_behavior]
+    c.obs_mode = N.OBS[o.mode]
+    c.n_rays = o.n_rays
+    c.max_agents_obs = o.max_agents_obs
+    c.max_road_points_obs = o.max_road_points_obs
+    c.obs_width = obs_width(o)
+    c.radius, c.fov, c.max_range = o.radius, o.fov, o.max_range
+    c.goal_tolerance = cfg.goal_tolerance
+    c.accel_lo, c.accel_hi = cfg.accel_bounds
+    c.steer_lo, c.steer_hi = cfg.steer_bounds
+    c.v_max = cfg.v_max
+    for k in range(3):
+        c.delta_lo[k], c.delta_hi[k] = cfg.delta_bounds[k]
+    c.grid_cell = grid_cell
+    return c
+
+
+def default_grid_cell(obs: ObsConfig) -> float:
+    """Cell edge of the static road grid: ~radius/6 for radial queries."""
+    return 8.0 if obs.mode == "radial" else 10.0
+
+
+class _WorldView:
+    """Read-only snapshot view of one world (the attributes tests read from
+    reference World objects: t, controlled_ids, replay tables, dt ...)."""
+
+    def __init__(self, batch: "SimBatch", w: int):
+        self._b = batch
+        self.world_id = w
+        pw = batch.packed
+        self.name = pw.names[w]
+        self.dt = float(pw.dt[w])
+        self.num_steps = int(pw.num_steps[w])
+        self.n_agents = int(pw.a_off[w + 1] - pw.a_off[w])
+        self.controlled_ids = pw.controlled_ids(w)
+        self.n_controlled = len(self.controlled_ids)
+        self.n_instantiated = int(pw.n_instantiated[w])
+        A, T, r0 = self.n_agents, self.num_steps, int(pw.r_off[w])
+        sl = slice(r0, r0 + A * T)
+        self.replay_pos = np.stack([pw.rep_x[sl].reshape(T, A).T, pw.rep_y[sl].reshape(T, A).T], -1)
+        self.replay_heading = pw.rep_h[sl].reshape(T, A).T
+        self.replay_speed = pw.rep_v[sl].reshape(T, A).T
+
+    def _agents(self, arr: torch.Tensor) -> np.ndarray:
+        pw = self._b.packed
+        return arr[int(pw.a_off[self.world_id]):int(pw.a_off[self.world_id + 1])].cpu().numpy()
+
+    @property
+    def t(self) -> int:
+        return int(self._b._t[self.world_id].item())
+
+    @property
+    def episode_over(self) -> bool:
+        return bool(self._b._over[self.world_id].item())
+
+    @property
+    def pos(self) -> np.ndarray:
+        return np.stack([self._agents(self._b._x), self._agents(self._b._y)], -1)
+
+    @property
+    def heading(self) -> np.ndarray:
+        return self._agents(self._b._h)
+
+    @property
+    def speed(self) -> np.ndarray:
+        return self._agents(self._b._v)
+
+    @property
+    def head_angle(self) -> np.ndarray:
+        return self._agents(self._b._head)
+
+    def _flag(self, bit) -> np.ndarray:
+        return (self._agents(self._b._flags).astype(np.int64) & bit) != 0
+
+    present = property(lambda s: s._flag(N.F_PRESENT))
+    removed = property(lambda s: s._flag(N.F_REMOVED))
+    done = property(lambda s: s._flag(N.F_DONE))
+    collided_now = property(lambda s: s._flag(N.F_COLLIDED))
+    offroad_now = property(lambda s: s._flag(N.F_OFFROAD))
+    goal_reached = property(lambda s: s._flag(N.F_GOAL_REACHED))
+
+
+def _dev(a: np.ndarray, device, dtype=None) -> torch.Tensor:
+    a = np.ascontiguousarray(a)
+    if a.size == 0:   # keep a valid, non-null pointer for empty tables
+        a = np.zeros(1, a.dtype)
+    t = torch.from_numpy(a)
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(device)
+
+
+class SimBatch:
+    """W independent worlds stepped in lockstep on one CUDA device.
+
+    ``SimBatch(scenarios, cfg)`` takes prepared scenarios (ours or the
+    reference's objects); ``SimBatch.from_raw(raw, cfg)`` takes a vectorised
+    ``RawWorlds`` batch (the synthetic generator's output) without building
+    per-object Python lists.
+    """
+
+    RING_STEPS = 64   # episode-ring capacity in steps of n_worlds records
+
+    def __init__(self, scenarios: list, cfg: SimConfig, n_workers: int = 1,
+                 device=None, grid_cell: float | None = None, _raw: RawWorlds | None = None):
+        if _raw is None:
+            if not scenarios:
+                raise ValueError("need at least one scenario")
+            _raw = raw_from_prepared(scenarios)
+        self.cfg = cfg
+        self.device = torch.device(device if device is not None else "cuda")
+        if self.device.type != "cuda":
+            raise ValueError("the B200 SimBatch runs on a CUDA device only (no CPU fallback)")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.packed: PackedWorlds = pack(_raw, cfg)
+        pw = self.packed
+        self.n_worlds = pw.n_worlds
+        self.offsets = pw.c_off.copy()
+        self.n_controlled = pw.n_controlled
+        self.total_agents = int(pw.n_instantiated.sum())
+        self.width = obs_width(cfg.obs)
+        for w in np.nonzero(np.diff(pw.c_off) == 0)[0]:
+            warnings.warn(f"world {w} ({pw.names[w]}): no controllable agents, replay-only",
+                          NoControllableAgents)
+        self.agent_index = [(int(w), int(a)) for w in range(self.n_worlds)
+                            for a in pw.controlled_ids(w)] if self.n_controlled < 200_000 else None
+        self.grid_cell = grid_cell or default_grid_cell(cfg.obs)
+        self.layout: DeviceLayout = build_layout(pw, self.grid_cell)
+        self._upload()
+        self._episode_infos: list = []
+        self._serial = 0
+        self._steps_since_drain = 0
+        self._handle = C.c_void_p()
+        N.check(N.lib().ds_create(C.byref(self._tables), C.byref(self._cfg_native),
+                                  C.byref(self._state), self.device.index,
+                                  C.byref(self._handle)), "ds_create")
+        self._closed = False
+        self.reset()
+
+    @classmethod
+    def from_raw(cls, raw: RawWorlds, cfg: SimConfig, device=None,
+                 grid_cell: float | None = None) -> "SimBatch":
+        return cls([], cfg, device=device, grid_cell=grid_cell, _raw=raw)
+
+    # -- construction ------------------------------------------------------
+
+    def _upload(self):
+        pw, lay, dev = self.packed, self.layout, self.device
+        A = np.diff(pw.a_off)
+        self.max_agents = int(A.max()) if len(A) else 0
+        t = {}
+        t["a_off"] = _dev(pw.a_off, dev)
+        t["c_off"] = _dev(pw.c_off, dev)
+        t["r_off"] = _dev(pw.r_off, dev)
+        t["num_steps"] = _dev(pw.num_steps.astype(np.int32), dev)
+        t["dt"] = _dev(pw.dt, dev)
+        for name in ("kind", "length", "width", "half_l", "half_w", "circumradius", "goal_x",
+                     "goal_y", "sflags", "ctrl_row", "row_agent", "rep_x", "rep_y", "rep_h",
+                     "rep_v", "rep_valid", "rep_present"):
+            t[name] = _dev(getattr(pw, name), dev)
+        for name in ("grid_x0", "grid_y0", "grid_nx", "grid_ny", "grid_cell_off",
+                     "pt_cell_start", "gpt_x", "gpt_y", "gpt_h", "gpt_kind", "gpt_id",
+                     "eseg_cell_start", "eseg_ax", "eseg_ay", "eseg_bx", "eseg_by",
+                     "aseg_cell_start", "aseg_ax", "aseg_ay", "aseg_bx", "aseg_by", "aseg_id",
+                     "aseg_edge"):
+            t[name] = _dev(getattr(lay, name), dev)
+        t["p_off"] = _dev(pw.p_off, dev)
+        t["s_off"] = _dev(pw.s_off, dev)
+        self._t_tensors = t
+        tab = N.DsTables()
+        tab.n_worlds = pw.n_worlds
+        tab.n_agents = pw.n_agents
+        tab.n_rows = pw.n_controlled
+        tab.max_agents = self.max_agents
+        for name in N.TABLE_PTRS:
+            setattr(tab, name, t[name].data_ptr())
+        self._tables = tab
+        self._cfg_native = make_native_config(self.cfg, self.grid_cell)
+
+        n, W, nc = pw.n_agents, pw.n_worlds, pw.n_controlled
+        f64 = dict(dtype=torch.float64, device=dev)
+        self._x = torch.zeros(max(n, 1), **f64)
+        self._y = torch.zeros(max(n, 1), **f64)
+        self._h = torch.zeros(max(n, 1), **f64)
+        self._v = torch.zeros(max(n, 1), **f64)
+        self._head = torch.zeros(max(n, 1), **f64)
+        self._flags = torch.zeros(max(n, 1), dtype=torch.int16, device=dev)
+        self._t = torch.zeros(W, dtype=torch.int32, device=dev)
+        self._over = torch.zeros(W, dtype=torch.uint8, device=dev)
+        self._ring_cap = max(1024, self.RING_STEPS * W)
+        self._ring = torch.zeros(self._ring_cap * 6, dtype=torch.int32, device=dev)
+        self._ring_head = torch.zeros(1, dtype=torch.int32, device=dev)
+        st = N.DsState()
+        for name, ten in (("x", self._x), ("y", self._y), ("heading", self._h),
+                          ("speed", self._v), ("head_angle", self._head),
+                          ("flags", self._flags), ("t", self._t), ("episode_over", self._over),
+                          ("ring", self._ring), ("ring_head", self._ring_head)):
+            setattr(st, name, ten.data_ptr())
+        st.ring_cap = self._ring_cap
+        self._state = st
+
+        # Outputs (reused every call, like the reference's buffers).
+        self.observations = torch.zeros((max(nc, 1), self.width), dtype=torch.float32,
+                                        device=dev)[:nc]
+        self.rewards = torch.zeros(max(nc, 1), dtype=torch.float32, device=dev)[:nc]
+        self.dones = torch.zeros(max(nc, 1), dtype=torch.bool, device=dev)[:nc]
+        self._info = torch.zeros((3, max(nc, 1)), dtype=torch.bool, device=dev)
+        self.info = {k: self._info[i, :nc] for i, k in
+                     enumerate(("goal", "veh_collision", "offroad"))}
+        self._mask = torch.zeros(W, dtype=torch.uint8, device=dev)
+
+    # -- stepping ----------------------------------------------------------
+
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _maybe_drain(self):
+        if (self._steps_since_drain + 1) * self.n_worlds > self._ring_cap:
+            self._drain()
+
+    def step(self, actions, *, sel_idx: torch.Tensor | None = None,
+             obs_scale: torch.Tensor | None = None, auto_reset: bool = False,
+             action_idx: torch.Tensor | None = None, grid=None) -> StepOutput:
+        """One step of every world; ``actions`` has one row per controlled
+        agent (flat over worlds) or is None for expert replay everywhere."""
+        self._check_open()
+        a = N.DsStepArgs()
+        keep = []
+        if action_idx is not None:
+            idx = torch.as_tensor(action_idx, device=self.device).to(torch.int32).contiguous()
+            if idx.shape[0] != self.n_controlled:
+                raise ActionCountMismatch(
+                    f"expected {self.n_controlled} action rows, got {idx.shape[0]}")
+            accel, steer = grid
+            a.action_idx = idx.data_ptr()
+            a.grid_accel = accel.data_ptr()
+            a.grid_steer = steer.data_ptr()
+            a.n_accel = accel.numel()
+            a.n_steer = steer.numel()
+            keep += [idx]
+        elif actions is None:
+            a.replay = 1
+        else:
+            act = torch.as_tensor(actions)
+            if act.ndim != 2 or act.shape[0] != self.n_controlled:
+                n_got = act.shape[0] if act.ndim else 0
+                raise ActionCountMismatch(
+                    f"expected {self.n_controlled} action rows, got {n_got}")
+            act = act.to(device=self.device, dtype=torch.float32).contiguous()
+            a.actions = act.data_ptr()
+            a.act_dim = act.shape[1]
+            keep.append(act)
+        self._maybe_drain()
+        a.obs = self.observations.data_ptr()
+        a.rewards = self.rewards.data_ptr()
+        a.dones = self.dones.data_ptr()
+        a.info = self._info.data_ptr()
+        a.obs_scale = obs_scale.data_ptr() if obs_scale is not None else None
+        a.auto_reset = 1 if auto_reset else 0
+        a.serial = self._serial
+        a.sel_idx = sel_idx.data_ptr() if sel_idx is not None else None
+        N.check(N.lib().ds_step(self._handle, C.byref(a), self._stream()), "ds_step")
+        self._serial += 1
+        self._steps_since_drain += 1
+        return StepOutput(self.observations, self.rewards, self.dones, self.info)
+
+    def reset(self, world_ids=None, *, obs_scale: torch.Tensor | None = None,
+              sel_idx: torch.Tensor | None = None, world_mask: torch.Tensor | None = None):
+        """engine.py:651-663: reset the given worlds (all by default) and
+        recompute their observation rows; their rewards/dones rows read 0."""
+        self._check_open()
+        mask_ptr = None
+        if world_mask is not None:
+            mask_ptr = world_mask.to(torch.uint8).contiguous().data_ptr()
+        elif world_ids is not None:
+            ids = torch.as_tensor(list(world_ids) if not torch.is_tensor(world_ids) else world_ids,
+                                  dtype=torch.int64)
+            self._mask.zero_()
+            if ids.numel():
+                self._mask[ids.to(self.device)] = 1
+            mask_ptr = self._mask.data_ptr()
+        N.check(N.lib().ds_reset(self._handle, mask_ptr, self.observations.data_ptr(),
+                                 self.rewards.data_ptr(), self.dones.data_ptr(),
+                                 obs_scale.data_ptr() if obs_scale is not None else None,
+                                 sel_idx.data_ptr() if sel_idx is not None else None,
+                                 self._stream()), "ds_reset")
+        return self.observations
+
+    def observe(self, obs_scale=None, sel_idx=None):
+        N.check(N.lib().ds_observe(self._handle, None, self.observations.data_ptr(),
+                                   obs_scale.data_ptr() if obs_scale is not None else None,
+                                   sel_idx.data_ptr() if sel_idx is not None else None,
+                                   self._stream()), "ds_observe")
+        return self.observations
+
+    # -- episode records ---------------------------------------------------
+
+    def _drain(self):
+        buf = np.zeros((self._ring_cap, 6), np.int32)
+        n = C.c_int32(0)
+        rc = N.lib().ds_episode_drain(self._handle, buf.ctypes.data_as(C.c_void_p),
+                                      self._ring_cap, C.byref(n), self._stream())
+        self._steps_since_drain = 0
+        recs = buf[:n.value]
+        if len(recs):
+            recs = recs[np.lexsort((recs[:, 1], recs[:, 0]))]
+            names = self.packed.names
+            for serial, w, nc, ng, nv, no in recs.tolist():
+                self._episode_infos.append(EpisodeInfo(names[w], w, nc, ng, nv, no))
+        N.check(rc, "ds_episode_drain")
+
+    @property
+    def episode_infos(self) -> list:
+        """Finished-episode records in (step, world) order (synchronises)."""
+        self._drain()
+        return self._episode_infos
+
+    @property
+    def episode_over(self) -> torch.Tensor:
+        return self._over.bool()
+
+    def compute_metrics(self) -> Metrics:
+        return compute_metrics(self.episode_infos)
+
+    @property
+    def worlds(self) -> list:
+        return [_WorldView(self, w) for w in range(self.n_worlds)]
+
+    def _slice(self, w: int) -> slice:
+        return slice(int(self.offsets[w]), int(self.offsets[w + 1]))
+
+    # -- lifecycle ---------------------------------------------------------
+
+    def _check_open(self):
+        if self._closed:
+            raise RuntimeError("SimBatch is closed")
+
+    def close(self):
+        if not getattr(self, "_closed", True):
+            torch.cuda.synchronize(self.device)
+            N.lib().ds_destroy(self._handle)
+            self._closed = True
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def init_batch(scenarios: list, cfg: SimConfig, n_workers: int = 1, device=None) -> SimBatch:
+    """engine.py:788."""
+    return SimBatch(scenarios, cfg, n_workers=n_workers, device=device)
+
+
+def random_actions(n_rows: int, cfg: SimConfig, seed: int, t: int, device) -> torch.Tensor:
+    """Counter-based uniform actions over the config bounds:
+    a pure function of (seed, row, t), so shard-invariant."""
+    g = torch.Generator(device=device)
+    g.manual_seed((int(seed) * 1_000_003 + int(t)) & 0x7FFFFFFFFFFFFFFF)
+    cols = cfg.action_dim
+    u = torch.rand((n_rows, cols), generator=g, device=device, dtype=torch.float32)
+    if cfg.dynamics == "delta_local":
+        lo = torch.tensor([b[0] for b in cfg.delta_bounds], device=device, dtype=torch.float32)
+        hi = torch.tensor([b[1] for b in cfg.delta_bounds], device=device, dtype=torch.float32)
+    else:
+        lo = torch.tensor([cfg.accel_bounds[0], cfg.steer_bounds[0]], device=device,
+                          dtype=torch.float32)
+        hi = torch.tensor([cfg.accel_bounds[1], cfg.steer_bounds[1]], device=device,
+                          dtype=torch.float32)
+    return lo + (hi - lo) * u
+
+
+def benchmark(scenarios: list, cfg: SimConfig, worlds: int, steps: int, policy: str = "random",
+              n_workers=None, seed: int | None = None, device=None) -> ThroughputReport:
+    """engine.py:811-857 on the GPU: step ``worlds`` worlds ``steps`` times
+    under a trivial policy with observations every step and auto-reset;
+    elapsed time from CUDA events (init/upload excluded)."""
+    if worlds < 1 or steps < 1:
+        raise ValueError("worlds and steps must be >= 1")
+    seed = cfg.seed if seed is None else seed
+    chosen = [scenarios[w % len(scenarios)] for w in range(worlds)]
+    batch = SimBatch(chosen, cfg, device=device)
+    dev = batch.device
+    acts = None
+    if policy == "random":
+        acts = [random_actions(batch.n_controlled, cfg, seed, t, dev) for t in range(min(steps, 8))]
+    elif policy.startswith("constant"):
+        parts = policy.split(":")
+        a = float(parts[1]) if len(parts) > 1 else 0.0
+        s = float(parts[2]) if len(parts) > 2 else 0.0
+        acts = [torch.tensor([[a, s]], device=dev).repeat(batch.n_controlled, 1)]
+    elif policy != "replay":
+        raise ValueError(f"unknown policy {policy!r}")
+    torch.cuda.synchronize(dev)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for t in range(steps):
+        batch.step(None if acts is None else acts[t % len(acts)], auto_reset=True)
+    end.record()
+    torch.cuda.synchronize(dev)
+    elapsed = start.elapsed_time(end) / 1e3
+    rep = ThroughputReport(worlds=worlds, steps=steps, elapsed_s=elapsed,
+                           total_agents=batch.total_agents,
+                           controlled_agents=batch.n_controlled)
+    batch.close()
+    return rep

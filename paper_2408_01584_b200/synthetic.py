@@ -1,0 +1,182 @@
+"""Waymo-shaped synthetic scenes, generated vectorised.
+
+The reference's own templates (pkg/src/drivesim/synthetic.py) cap at 24/12/25
+agents with a handful of road points, so they cannot produce the benchmark
+configurations (32-128 agents, 400-10k road points).  This generator follows
+the survey's recipe:
+
+* map side L = 40*sqrt(P/100) + 60 m;
+* road polylines of 10-60 points at 2 m spacing with a heading random walk
+  (sigma 0.05 rad/point), exactly P points per world; kinds lane 40 %,
+  road_edge 30 %, road_line 20 %, crosswalk 10 %;
+* agents 80 % vehicle (4.6 +- 0.3 x 1.8 m), 10 % pedestrian (0.8 x 0.8),
+  10 % cyclist (1.8 x 0.6), uniform in the central L/2 square, heading
+  U(-pi, pi], speed U[2, 15] m/s;
+* T-step logs from a classic-bicycle rollout with a = 0 and a constant steer
+  U(-0.1, 0.1), all valid; goal = final logged position;
+* every coordinate quantised to 2^-10 m (lossless in float32).
+
+A world's content depends only on (seed, global world id), so a world shard
+generated on any rank is identical to the same world generated anywhere else.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .config import OBJECT_KINDS, ROAD_KINDS
+from .packing import RawWorlds, _offsets
+
+Q = 1.0 / 1024.0
+KIND_P = {"lane": 0.4, "road_edge": 0.3, "road_line": 0.2, "crosswalk": 0.1}
+
+
+@dataclass
+class WaymoSpec:
+    n_worlds: int
+    n_agents: int = 32
+    n_points: int = 400
+    seed: int = 0
+    num_steps: int = 91
+    dt: float = 0.1
+    world_offset: int = 0       # global id of the first world (sharding)
+    map_side: float | None = None
+
+    @property
+    def side(self) -> float:
+        if self.map_side is not None:
+            return self.map_side
+        return 40.0 * math.sqrt(self.n_points / 100.0) + 60.0
+
+
+def _quant(v):
+    return np.round(np.asarray(v) / Q) * Q
+
+
+def _world(spec: WaymoSpec, wid: int):
+    rng = np.random.default_rng([spec.seed, wid])
+    L = spec.side
+    A, T, P = spec.n_agents, spec.num_steps, spec.n_points
+    # ---- agents
+    u = rng.random(A)
+    kind = np.where(u < 0.8, 0, np.where(u < 0.9, 1, 2)).astype(np.int8)
+    length = np.where(kind == 0, 4.6 + rng.uniform(-0.3, 0.3, A), np.where(kind == 1, 0.8, 1.8))
+    width = np.where(kind == 0, 1.8, np.where(kind == 1, 0.8, 0.6))
+    x = _quant(rng.uniform(0.25 * L, 0.75 * L, A))
+    y = _quant(rng.uniform(0.25 * L, 0.75 * L, A))
+    h = -rng.uniform(-math.pi, math.pi, A)          # (-pi, pi]
+    v = rng.uniform(2.0, 15.0, A)
+    steer = rng.uniform(-0.1, 0.1, A)
+    beta = np.arctan(0.5 * np.tan(steer))
+    lx = np.empty((A, T)); ly = np.empty((A, T)); lh = np.empty((A, T))
+    cx, cy, ch = x.copy(), y.copy(), h.copy()
+    for t in range(T):
+        lx[:, t], ly[:, t], lh[:, t] = _quant(cx), _quant(cy), ch
+        cx = cx + v * np.cos(ch + beta) * spec.dt
+        cy = cy + v * np.sin(ch + beta) * spec.dt
+        ch = np.mod(ch + v * np.cos(beta) * np.tan(steer) / length * spec.dt + math.pi,
+                    2 * math.pi) - math.pi
+        ch = np.where(ch <= -math.pi, ch + 2 * math.pi, ch)
+    vx = v[:, None] * np.cos(lh)
+    vy = v[:, None] * np.sin(lh)
+    goal = np.stack([lx[:, -1], ly[:, -1]], -1)
+    # ---- roads: polylines of 10..60 points summing to exactly P
+    lens = []
+    left = P
+    while left > 0:
+        n = int(rng.integers(10, 61))
+        if left - n < 10:
+            n = left
+        lens.append(n)
+        left -= n
+    lens = np.array(lens, np.int64)
+    R = len(lens)
+    ku = rng.random(R)
+    cum = np.cumsum([KIND_P["road_edge"], KIND_P["lane"], KIND_P["road_line"]])
+    kinds = np.where(ku < cum[0], ROAD_KINDS.index("road_edge"),
+                     np.where(ku < cum[1], ROAD_KINDS.index("lane"),
+                              np.where(ku < cum[2], ROAD_KINDS.index("road_line"),
+                                       ROAD_KINDS.index("crosswalk")))).astype(np.int8)
+    start = rng.uniform(0.0, L, (R, 2))
+    h0 = rng.uniform(-math.pi, math.pi, R)
+    steps = rng.normal(0.0, 0.05, P)
+    poly_of = np.repeat(np.arange(R), lens)
+    first = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    steps[first] = 0.0
+    ang = np.cumsum(steps)
+    ang = ang - np.repeat(ang[first], lens) + h0[poly_of]
+    dx = 2.0 * np.cos(ang)
+    dy = 2.0 * np.sin(ang)
+    dx[first] = 0.0
+    dy[first] = 0.0
+    px = np.cumsum(dx); py = np.cumsum(dy)
+    px = px - np.repeat(px[first], lens) + start[poly_of, 0]
+    py = py - np.repeat(py[first], lens) + start[poly_of, 1]
+    return dict(kind=kind, length=length, width=width, goal=_quant(goal), lx=lx, ly=ly, lh=lh,
+                vx=vx, vy=vy, lens=lens, pkind=kinds, px=_quant(px), py=_quant(py))
+
+
+def generate(spec: WaymoSpec) -> RawWorlds:
+    """RawWorlds for worlds [world_offset, world_offset + n_worlds)."""
+    parts = [_world(spec, spec.world_offset + k) for k in range(spec.n_worlds)]
+    W, A, T = spec.n_worlds, spec.n_agents, spec.num_steps
+    cat = lambda key: np.concatenate([p[key] for p in parts])
+    lens = [p["lens"] for p in parts]
+    raw = RawWorlds(
+        names=[f"waymo-synth-{spec.seed}-{spec.world_offset + k}" for k in range(W)],
+        dt=np.full(W, spec.dt), num_steps=np.full(W, T, np.int32),
+        a_off=_offsets([A] * W), kind=cat("kind"), length=cat("length"),
+        width=cat("width"), goal=cat("goal").reshape(-1, 2),
+        force_replay=np.zeros(W * A, bool), controllable=np.zeros(W * A, bool),
+        l_off=_offsets([A * T] * W), log_x=cat("lx").reshape(-1), log_y=cat("ly").reshape(-1),
+        log_h=cat("lh").reshape(-1), log_vx=cat("vx").reshape(-1), log_vy=cat("vy").reshape(-1),
+        log_valid=np.ones(W * A * T, bool),
+        poly_off=_offsets([len(l) for l in lens]), poly_kind=cat("pkind"),
+        poly_pt_off=_offsets(np.concatenate(lens)), pt_x=cat("px"), pt_y=cat("py"))
+    # mark_controllable (scenario.py:371-384) with the default 2.0 m threshold
+    sx = raw.log_x.reshape(-1, T)[:, 0]
+    sy = raw.log_y.reshape(-1, T)[:, 0]
+    d = _native.host_hypot_cpython(sx - raw.goal[:, 0], sy - raw.goal[:, 1])
+    raw.controllable = d > 2.0
+    return raw
+
+
+def to_scenarios(raw: RawWorlds, types=None) -> list:
+    """Prepared-scenario objects for ``raw`` built with ``types`` (a module
+    exposing Vec2/LoggedStep/ObjectLog/RoadElement/Scenario/PreparedScenario/
+    PrepStats -- ours by default, or the reference's drivesim.scenario)."""
+    if types is None:
+        from . import scenario as types
+    out = []
+    for w in range(raw.n_worlds):
+        T = int(raw.num_steps[w])
+        objs = []
+        for k, g in enumerate(range(raw.a_off[w], raw.a_off[w + 1])):
+            base = raw.l_off[w] + k * T
+            states = [types.LoggedStep(position=types.Vec2(float(raw.log_x[base + t]),
+                                                           float(raw.log_y[base + t])),
+                                       heading=float(raw.log_h[base + t]),
+                                       velocity=types.Vec2(float(raw.log_vx[base + t]),
+                                                           float(raw.log_vy[base + t])),
+                                       valid=bool(raw.log_valid[base + t])) for t in range(T)]
+            objs.append(types.ObjectLog(id=k, kind=OBJECT_KINDS[raw.kind[g]],
+                                        length=float(raw.length[g]), width=float(raw.width[g]),
+                                        goal=types.Vec2(float(raw.goal[g, 0]), float(raw.goal[g, 1])),
+                                        states=states, force_replay=bool(raw.force_replay[g])))
+        roads = []
+        for rid, r in enumerate(range(raw.poly_off[w], raw.poly_off[w + 1])):
+            pts = [types.Vec2(float(raw.pt_x[q]), float(raw.pt_y[q]))
+                   for q in range(raw.poly_pt_off[r], raw.poly_pt_off[r + 1])]
+            roads.append(types.RoadElement(id=rid, kind=ROAD_KINDS[raw.poly_kind[r]], geometry=pts))
+        s = types.Scenario(name=raw.names[w], timestep=float(raw.dt[w]), num_steps=T,
+                           objects=objs, roads=roads)
+        ctrl = [bool(c) for c in raw.controllable[raw.a_off[w]:raw.a_off[w + 1]]]
+        n_pts = sum(len(r.geometry) for r in roads)
+        out.append(types.PreparedScenario(
+            base=s, decimated_roads=roads, controllable=ctrl,
+            stats=types.PrepStats(len(objs), sum(ctrl), n_pts, n_pts)))
+    return out
