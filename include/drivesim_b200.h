@@ -161,11 +161,16 @@ typedef struct ds_step_args {
   int32_t serial;            /* step serial number recorded in the episode ring */
   int32_t *sel_idx;          /* debug/parity: [n_rows, max_agents_obs+max_road_points_obs] selected ids, or NULL */
   int32_t reserved0;
+  /* optional cudaEvent_t recorded on the stream: before the step kernel,
+   * between step and observation kernels, after the observation kernel */
+  void *events[3];
 } ds_step_args;
 
 typedef struct ds_handle ds_handle;
 
 int ds_abi_version(void);
+/* sizeof(ds_config), sizeof(ds_tables), sizeof(ds_state), sizeof(ds_step_args) */
+void ds_struct_sizes(int64_t out[4]);
 const char *ds_last_error(void);
 
 int ds_create(const ds_tables *tables, const ds_config *cfg, ds_state *state,

@@ -87,10 +87,10 @@ class DsStepArgs(C.Structure):
                 ("n_accel", C.c_int32), ("n_steer", C.c_int32), ("obs", _p),
                 ("rewards", _p), ("dones", _p), ("info", _p), ("obs_scale", _p),
                 ("auto_reset", C.c_int32), ("serial", C.c_int32), ("sel_idx", _p),
-                ("reserved0", C.c_int32)]
+                ("reserved0", C.c_int32), ("events", _p * 3)]
 
 
-EXPORTS = ["ds_abi_version", "ds_last_error", "ds_create", "ds_destroy", "ds_reset", "ds_step",
+EXPORTS = ["ds_abi_version", "ds_struct_sizes", "ds_last_error", "ds_create", "ds_destroy", "ds_reset", "ds_step",
            "ds_observe", "ds_episode_drain", "ds_host_hypot_libm", "ds_host_hypot_cpython",
            "ds_host_hypot_port", "ds_host_road_headings"]
 
@@ -107,6 +107,8 @@ def lib():
                           "(there is no CPU fallback for the batched step)")
     L = C.CDLL(LIB_PATH)
     L.ds_abi_version.restype = C.c_int
+    L.ds_struct_sizes.argtypes = [_p]
+    L.ds_struct_sizes.restype = None
     L.ds_last_error.restype = C.c_char_p
     L.ds_create.argtypes = [C.POINTER(DsTables), C.POINTER(DsConfig), C.POINTER(DsState),
                             C.c_int, C.POINTER(_p)]
@@ -119,10 +121,15 @@ def lib():
         getattr(L, n).argtypes = [_p, _p, C.c_int64, _p]
     L.ds_host_road_headings.argtypes = [_p, _p, _p, C.c_int64, _p]
     for n in EXPORTS:
-        if n not in ("ds_abi_version", "ds_last_error"):
+        if n not in ("ds_abi_version", "ds_last_error", "ds_struct_sizes"):
             getattr(L, n).restype = C.c_int
     if L.ds_abi_version() != ABI_VERSION:
         raise ImportError("libdrivesim_b200.so ABI version mismatch; rebuild")
+    sizes = (C.c_int64 * 4)()
+    L.ds_struct_sizes(sizes)
+    mine = (C.sizeof(DsConfig), C.sizeof(DsTables), C.sizeof(DsState), C.sizeof(DsStepArgs))
+    if tuple(sizes) != mine:
+        raise ImportError(f"C-ABI struct layout mismatch: lib {tuple(sizes)} vs ctypes {mine}")
     _lib = L
     return L
 

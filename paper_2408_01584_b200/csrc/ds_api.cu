@@ -35,6 +35,13 @@ extern "C" {
 
 int ds_abi_version(void) { return DS_ABI_VERSION; }
 
+void ds_struct_sizes(int64_t out[4]) {
+  out[0] = sizeof(ds_config);
+  out[1] = sizeof(ds_tables);
+  out[2] = sizeof(ds_state);
+  out[3] = sizeof(ds_step_args);
+}
+
 const char *ds_last_error(void) { return g_err; }
 
 int ds_create(const ds_tables *tables, const ds_config *cfg, ds_state *state, int device,
@@ -133,10 +140,17 @@ int ds_step(ds_handle *h, const ds_step_args *a, void *stream) {
     }
   }
   cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e = ds::launch_step(h, a, s);
+  cudaError_t e;
+  if (a->events[0] && (e = cudaEventRecord((cudaEvent_t)a->events[0], s)) != cudaSuccess)
+    return cuda_fail(e, "event");
+  e = ds::launch_step(h, a, s);
   if (e != cudaSuccess) return cuda_fail(e, "step_kernel");
+  if (a->events[1] && (e = cudaEventRecord((cudaEvent_t)a->events[1], s)) != cudaSuccess)
+    return cuda_fail(e, "event");
   e = ds::launch_observe(h, nullptr, a->obs, a->obs_scale, a->sel_idx, s);
   if (e != cudaSuccess) return cuda_fail(e, "observe kernel");
+  if (a->events[2] && (e = cudaEventRecord((cudaEvent_t)a->events[2], s)) != cudaSuccess)
+    return cuda_fail(e, "event");
   return DS_OK;
 }
 

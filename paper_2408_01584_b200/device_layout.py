@@ -22,7 +22,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .config import ROAD_EDGE
-from .packing import PackedWorlds
+from .packing import PackedWorlds, _offsets
 
 
 @dataclass
@@ -71,7 +71,7 @@ def _bin_segments(pw: PackedWorlds, sel: np.ndarray, world_of_seg: np.ndarray,
     nys = cy1 - cy0 + 1
     cnt = nxs * nys
     rep = np.repeat(np.arange(len(idx)), cnt)
-    k = np.arange(cnt.sum()) - np.repeat(np.concatenate([[0], np.cumsum(cnt)[:-1]]), cnt)
+    k = np.arange(cnt.sum()) - np.repeat(_offsets(cnt)[:-1], cnt)
     kx = k % np.repeat(nxs, cnt)
     ky = k // np.repeat(nxs, cnt)
     cells = (cell_base[w[rep]] + (cy0[rep] + ky) * nx[w[rep]] + (cx0[rep] + kx)).astype(np.int64)
@@ -83,7 +83,7 @@ def _bin_segments(pw: PackedWorlds, sel: np.ndarray, world_of_seg: np.ndarray,
     return start, idx[rep][order]
 
 
-def build_layout(pw: PackedWorlds, cell: float = 8.0) -> DeviceLayout:
+def build_layout(pw: PackedWorlds, cell: float = 8.0, all_segments: bool = True) -> DeviceLayout:
     W = pw.n_worlds
     P = np.diff(pw.p_off)
     world_of_pt = np.repeat(np.arange(W), P)
@@ -143,8 +143,9 @@ def build_layout(pw: PackedWorlds, cell: float = 8.0) -> DeviceLayout:
     edge = pw.seg_kind == ROAD_EDGE
     es, eorder = _bin_segments(pw, edge, world_of_seg, x0, y0, nx, ny, cell_base,
                                n_cells_total, cell)
-    as_, aorder = _bin_segments(pw, np.ones(len(world_of_seg), bool), world_of_seg, x0, y0, nx,
-                                ny, cell_base, n_cells_total, cell)
+    # all segments (LiDAR / view-cone rays); empty bins when the sensor is radial
+    as_, aorder = _bin_segments(pw, np.full(len(world_of_seg), bool(all_segments)), world_of_seg,
+                                x0, y0, nx, ny, cell_base, n_cells_total, cell)
     seg_local = np.arange(len(world_of_seg)) - np.repeat(pw.s_off[:-1], S)
     return DeviceLayout(
         cell=float(cell), grid_x0=x0.astype(np.float64), grid_y0=y0.astype(np.float64),

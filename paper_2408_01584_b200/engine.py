@@ -244,7 +244,8 @@ class SimBatch:
         self.agent_index = [(int(w), int(a)) for w in range(self.n_worlds)
                             for a in pw.controlled_ids(w)] if self.n_controlled < 200_000 else None
         self.grid_cell = grid_cell or default_grid_cell(cfg.obs)
-        self.layout: DeviceLayout = build_layout(pw, self.grid_cell)
+        self.layout: DeviceLayout = build_layout(pw, self.grid_cell,
+                                                  all_segments=cfg.obs.mode != "radial")
         self._upload()
         self._episode_infos: list = []
         self._serial = 0
@@ -339,7 +340,7 @@ class SimBatch:
 
     def step(self, actions, *, sel_idx: torch.Tensor | None = None,
              obs_scale: torch.Tensor | None = None, auto_reset: bool = False,
-             action_idx: torch.Tensor | None = None, grid=None) -> StepOutput:
+             action_idx: torch.Tensor | None = None, grid=None, events=None) -> StepOutput:
         """One step of every world; ``actions`` has one row per controlled
         agent (flat over worlds) or is None for expert replay everywhere."""
         self._check_open()
@@ -378,6 +379,9 @@ class SimBatch:
         a.auto_reset = 1 if auto_reset else 0
         a.serial = self._serial
         a.sel_idx = sel_idx.data_ptr() if sel_idx is not None else None
+        if events is not None:   # three torch.cuda.Event(enable_timing=True)
+            for k, ev in enumerate(events):
+                a.events[k] = ev.cuda_event
         N.check(N.lib().ds_step(self._handle, C.byref(a), self._stream()), "ds_step")
         self._serial += 1
         self._steps_since_drain += 1

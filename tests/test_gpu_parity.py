@@ -1,0 +1,113 @@
+"""GPU parity: the CUDA step (through the C ABI) against the C oracle, which is
+itself pinned bit-exact to the reference (tests/test_oracle_golden.py).
+
+Free-run over a full 91-step episode: rewards, dones, info flags and the
+partner / road-point selection indices must be bit-exact; observations within
+2 float32 ulp + 1e-5 of the FP64 oracle rounded to float32; poses within
+1e-9 m / 1e-11 rad (FP64 state; only transcendental ulps differ).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2408_01584_b200.config import ObsConfig, SimConfig
+from paper_2408_01584_b200.engine import SimBatch
+from paper_2408_01584_b200.synthetic import WaymoSpec, generate
+from oracle.oracle import OracleBatch
+from parity import ANG_TOL, POS_TOL, actions_for, compare_step, wrap_diff
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "c1_classic_remove": (dict(n_worlds=8, n_agents=32, n_points=400),
+                          dict(collision_behavior="remove_agent")),
+    "c1_invertible_ignore": (dict(n_worlds=8, n_agents=32, n_points=400),
+                             dict(dynamics="invertible")),
+    "c1_end_episode": (dict(n_worlds=8, n_agents=32, n_points=400),
+                       dict(collision_behavior="end_episode")),
+    "c1_delta_local": (dict(n_worlds=8, n_agents=32, n_points=400),
+                       dict(dynamics="delta_local", collision_behavior="remove_agent")),
+    "c2_shape": (dict(n_worlds=12, n_agents=64, n_points=2000),
+                 dict(collision_behavior="remove_agent")),
+    "c3_shape": (dict(n_worlds=3, n_agents=128, n_points=10000),
+                 dict(dynamics="delta_local")),
+    "small_caps": (dict(n_worlds=6, n_agents=40, n_points=900),
+                   dict(obs=ObsConfig(max_agents_obs=3, max_road_points_obs=5, radius=30.0))),
+    "big_caps": (dict(n_worlds=4, n_agents=100, n_points=6000),
+                 dict(obs=ObsConfig(max_agents_obs=128, max_road_points_obs=128, radius=80.0))),
+}
+
+
+def _gpu_out(batch):
+    return {"obs": batch.observations.cpu().numpy(), "rewards": batch.rewards.cpu().numpy(),
+            "dones": batch.dones.cpu().numpy(), "info": batch._info[:, :batch.n_controlled].cpu().numpy()}
+
+
+def run_free(case, steps=91, seed=0):
+    spec_kw, cfg_kw = CASES[case]
+    cfg = SimConfig(init_mode="all_valid", **cfg_kw)
+    raw = generate(WaymoSpec(seed=seed + 11, **spec_kw))
+    batch = SimBatch.from_raw(raw, cfg, device="cuda:0")
+    ora = OracleBatch(batch.packed, cfg)
+    n = batch.n_controlled
+    sel_w = cfg.obs.max_agents_obs + cfg.obs.max_road_points_obs
+    sel = torch.full((n, sel_w), -7, dtype=torch.int32, device="cuda:0")
+    batch.reset(sel_idx=sel)
+    compare_step(0, _gpu_out(batch), (ora.observations, ora.rewards, ora.dones.astype(bool),
+                                      {k: np.zeros(n, bool) for k in ("goal", "veh_collision", "offroad")}),
+                 sel.cpu().numpy(), ora.sel_idx[:n])
+    rng = np.random.default_rng(seed)
+    for t in range(1, steps + 1):
+        act = actions_for(cfg, n, rng)
+        batch.step(torch.from_numpy(act).cuda(), sel_idx=sel)
+        o = ora.step(act.astype(np.float64))
+        compare_step(t, _gpu_out(batch), o, sel.cpu().numpy(), ora.sel_idx[:n])
+    pw = batch.packed
+    x, y, h = batch._x.cpu().numpy(), batch._y.cpu().numpy(), batch._h.cpu().numpy()
+    nA = pw.n_agents
+    assert np.abs(x[:nA] - ora.x[:nA]).max() <= POS_TOL
+    assert np.abs(y[:nA] - ora.y[:nA]).max() <= POS_TOL
+    assert wrap_diff(h[:nA], ora.heading[:nA]).max() <= ANG_TOL
+    assert np.array_equal(batch._flags.cpu().numpy()[:nA].astype(np.uint16), ora.flags[:nA])
+    eps = [(e.world_id, e.n_controlled, e.n_goal, e.n_veh_collision, e.n_offroad)
+           for e in batch.episode_infos]
+    assert eps == ora.episode_infos
+    batch.close()
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_free_run_parity(case):
+    run_free(case)
+
+
+def test_replay_mode_parity():
+    """actions=None: expert replay for everyone (engine.py:383-385)."""
+    cfg = SimConfig(init_mode="all_valid")
+    raw = generate(WaymoSpec(n_worlds=4, n_agents=32, n_points=400, seed=5))
+    batch = SimBatch.from_raw(raw, cfg, device="cuda:0")
+    ora = OracleBatch(batch.packed, cfg)
+    for t in range(1, 92):
+        batch.step(None)
+        o = ora.step(None)
+        compare_step(t, _gpu_out(batch), o)
+    assert np.array_equal(batch._x.cpu().numpy(), ora.x)   # replay copies poses bit-exactly
+    batch.close()
+
+
+def test_auto_reset_env_semantics():
+    """auto_reset: finished worlds reset in-kernel, rewards rows zeroed (env.py:95-109)."""
+    cfg = SimConfig(init_mode="all_valid", collision_behavior="end_episode")
+    raw = generate(WaymoSpec(n_worlds=6, n_agents=32, n_points=400, seed=9))
+    batch = SimBatch.from_raw(raw, cfg, device="cuda:0")
+    ora = OracleBatch(batch.packed, cfg)
+    rng = np.random.default_rng(3)
+    for t in range(1, 200):
+        act = actions_for(cfg, batch.n_controlled, rng)
+        batch.step(torch.from_numpy(act).cuda(), auto_reset=True)
+        o = ora.step(act.astype(np.float64), auto_reset=True)
+        compare_step(t, _gpu_out(batch), o)
+    eps = [(e.world_id, e.n_controlled, e.n_goal, e.n_veh_collision, e.n_offroad)
+           for e in batch.episode_infos]
+    assert eps == ora.episode_infos and len(eps) > 6
+    batch.close()
