@@ -96,6 +96,7 @@ typedef struct ds_config {
  * CSR arrays of length n_worlds+1 unless noted. */
 typedef struct ds_tables {
   int32_t n_worlds, n_agents, n_rows, max_agents;
+  int32_t max_points, reserved0;    /* largest road-point count of a world */
   const int64_t *a_off, *c_off, *r_off;
   const int32_t *num_steps;
   const double *dt;
@@ -127,6 +128,10 @@ typedef struct ds_tables {
   const int32_t *aseg_id;           /* original segment index inside its world */
   const uint8_t *aseg_edge;         /* 1 if road_edge */
   const int64_t *s_off;             /* [n_worlds+1] segments per world (original) */
+  /* grid-sorted points as float2 relative to (grid_x0, grid_y0), and the
+   * per-world max |float - exact| of those coordinates (shared-memory scan) */
+  const float *gpt_xy;
+  const double *grid_eps;
 } ds_tables;
 
 /* Mutable simulation state (device pointers, torch-owned). */
@@ -201,6 +206,7 @@ int ds_episode_drain(ds_handle *h, int32_t *out, int32_t max_records,
 int ds_host_hypot_libm(const double *x, const double *y, int64_t n, double *out);
 int ds_host_hypot_cpython(const double *x, const double *y, int64_t n, double *out);
 int ds_host_hypot_port(const double *x, const double *y, int64_t n, double *out);
+int ds_host_wrap_port(const double *x, int64_t n, double *out);
 int ds_host_road_headings(const double *x, const double *y, const int64_t *poly_pt_off,
                           int64_t n_poly, double *out);
 

@@ -63,13 +63,14 @@ TABLE_PTRS = [
     "p_off", "pt_cell_start", "gpt_x", "gpt_y", "gpt_h", "gpt_kind", "gpt_id",
     "eseg_cell_start", "eseg_ax", "eseg_ay", "eseg_bx", "eseg_by",
     "aseg_cell_start", "aseg_ax", "aseg_ay", "aseg_bx", "aseg_by", "aseg_id", "aseg_edge",
-    "s_off",
+    "s_off", "gpt_xy", "grid_eps",
 ]
 
 
 class DsTables(C.Structure):
     _fields_ = ([("n_worlds", C.c_int32), ("n_agents", C.c_int32), ("n_rows", C.c_int32),
-                 ("max_agents", C.c_int32)] + [(n, _p) for n in TABLE_PTRS])
+                 ("max_agents", C.c_int32), ("max_points", C.c_int32), ("reserved0", C.c_int32)]
+                + [(n, _p) for n in TABLE_PTRS])
 
 
 STATE_PTRS = ["x", "y", "heading", "speed", "head_angle", "flags", "t", "episode_over",
@@ -92,7 +93,7 @@ class DsStepArgs(C.Structure):
 
 EXPORTS = ["ds_abi_version", "ds_struct_sizes", "ds_last_error", "ds_create", "ds_destroy", "ds_reset", "ds_step",
            "ds_observe", "ds_episode_drain", "ds_host_hypot_libm", "ds_host_hypot_cpython",
-           "ds_host_hypot_port", "ds_host_road_headings"]
+           "ds_host_hypot_port", "ds_host_wrap_port", "ds_host_road_headings"]
 
 _lib = None
 
@@ -120,6 +121,7 @@ def lib():
     for n in ("ds_host_hypot_libm", "ds_host_hypot_cpython", "ds_host_hypot_port"):
         getattr(L, n).argtypes = [_p, _p, C.c_int64, _p]
     L.ds_host_road_headings.argtypes = [_p, _p, _p, C.c_int64, _p]
+    L.ds_host_wrap_port.argtypes = [_p, C.c_int64, _p]
     for n in EXPORTS:
         if n not in ("ds_abi_version", "ds_last_error", "ds_struct_sizes"):
             getattr(L, n).restype = C.c_int
@@ -173,6 +175,13 @@ def host_hypot_port(x, y) -> np.ndarray:
     x, y = _f64(x), _f64(y)
     out = np.empty_like(x)
     check(lib().ds_host_hypot_port(_ptr(x), _ptr(y), x.size, _ptr(out)), "hypot_port")
+    return out
+
+
+def host_wrap_port(x) -> np.ndarray:
+    x = _f64(x)
+    out = np.empty_like(x)
+    check(lib().ds_host_wrap_port(_ptr(x), x.size, _ptr(out)), "wrap_port")
     return out
 
 

@@ -59,6 +59,9 @@ int ds_create(const ds_tables *tables, const ds_config *cfg, ds_state *state, in
       c.max_road_points_obs > ds::kSelCap)
     return fail(DS_E_CAPACITY, "slot caps must be in [0, %d]", ds::kSelCap);
   if (!(c.grid_cell > 0.0)) return fail(DS_E_INVALID, "grid_cell must be > 0");
+  if (c.obs_mode == DS_OBS_RADIAL && 2.0 * (c.radius + 1e-6) / c.grid_cell + 2.0 > 32.0)
+    return fail(DS_E_INVALID, "grid_cell %.3f too small for radius %.3f (> 32 cell rows)",
+                c.grid_cell, c.radius);
   if (tables->max_agents < 0 || tables->max_agents > DS_MAX_AGENTS_PER_WORLD)
     return fail(DS_E_CAPACITY, "max agents per world %d > %d", tables->max_agents,
                 DS_MAX_AGENTS_PER_WORLD);
@@ -80,10 +83,9 @@ int ds_create(const ds_tables *tables, const ds_config *cfg, ds_state *state, in
   int amax = tables->max_agents < 1 ? 1 : tables->max_agents;
   h->step_threads = ((amax + 31) / 32) * 32;
   h->step_smem = ds::step_smem_bytes(amax);
-  h->obs_warps = 8;
-  h->obs_smem = ds::obs_smem_bytes(c, amax, h->obs_warps, c.obs_width);
   int max_optin = 0;
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  ds::obs_plan(h, max_optin);
   if ((int)h->obs_smem > max_optin || (int)h->step_smem > max_optin) {
     delete h;
     return fail(DS_E_CAPACITY, "shared memory %zu/%zu exceeds %d", h->obs_smem, h->step_smem,
@@ -186,6 +188,11 @@ int ds_episode_drain(ds_handle *h, int32_t *out, int32_t max_records, int32_t *n
 
 int ds_host_hypot_libm(const double *x, const double *y, int64_t n, double *out) {
   for (int64_t i = 0; i < n; ++i) out[i] = ::hypot(x[i], y[i]);
+  return DS_OK;
+}
+
+int ds_host_wrap_port(const double *x, int64_t n, double *out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = ds::wrap(x[i]);
   return DS_OK;
 }
 

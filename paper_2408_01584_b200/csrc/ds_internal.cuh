@@ -16,23 +16,22 @@ struct ds_handle {
   int step_threads;     // threads per world CTA in the step kernel
   size_t step_smem;     // dynamic shared memory of the step kernel
   int obs_warps;        // warps per world CTA in the observation kernel
+  int obs_shared_pts;   // 1: road points staged in shared memory
   size_t obs_smem;
   uint32_t ring_read;   // host mirror of entries already drained
 };
 
 namespace ds {
 
-// Sizes of the per-warp selection scratch in the radial observation kernel.
-constexpr int kCandCap = 384;   // candidates kept before a streaming compaction
-constexpr int kSelCap = 128;    // bucket-threshold survivors sorted exactly
-constexpr int kBuckets = 256;   // first-level distance histogram
+// Largest supported max_agents_obs / max_road_points_obs (selection set size).
+constexpr int kSelCap = 128;
 
 cudaError_t launch_step(const ds_handle *h, const ds_step_args *a, cudaStream_t s);
 cudaError_t launch_reset(const ds_handle *h, const uint8_t *mask, float *rewards,
                          uint8_t *dones, cudaStream_t s);
 cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, float *obs,
                            const float *inv_scale, int32_t *sel_idx, cudaStream_t s);
-size_t obs_smem_bytes(const ds_config &cfg, int max_agents, int warps, int obs_width);
+void obs_plan(ds_handle *h, int max_dynamic_smem);
 size_t step_smem_bytes(int max_agents);
 cudaError_t configure_kernels(int max_dynamic_smem);
 cudaError_t configure_step_kernels(int max_dynamic_smem);

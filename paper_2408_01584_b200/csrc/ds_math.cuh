@@ -22,11 +22,21 @@ constexpr double kTwoPi = 6.283185307179586;   // 2.0 * math.pi (exact doubling)
 // (geo:70-72): r = (theta + pi) mod 2pi - pi with Python's floor-mod sign
 // rule, then +2pi if r <= -pi.  fmod is exact, so this is bit-reproducible.
 DS_HD double wrap(double theta) {
-  double r = fmod(theta + kPi, kTwoPi);
-  if (r != 0.0) {
-    if (r < 0.0) r += kTwoPi;
+  const double a = theta + kPi;
+  double r;
+  if (a >= 0.0 && a < kTwoPi) {
+    r = a;                      // fmod(a, 2pi) == a
+  } else if (a >= kTwoPi && a < 2.0 * kTwoPi) {
+    r = a - kTwoPi;             // exact (Sterbenz), == fmod(a, 2pi)
+  } else if (a < 0.0 && a >= -kTwoPi) {
+    r = a + kTwoPi;             // fmod(a, 2pi) == a < 0, then += 2pi
   } else {
-    r = 0.0;  // copysign(0, 2pi)
+    r = fmod(a, kTwoPi);
+    if (r != 0.0) {
+      if (r < 0.0) r += kTwoPi;
+    } else {
+      r = 0.0;  // copysign(0, 2pi)
+    }
   }
   r = r - kPi;
   if (r <= -kPi) r += kTwoPi;

@@ -1,180 +1,110 @@
-// ds_obs.cu -- observation kernels (World._fill_obs, engine.py:500-512).
+// ds_obs.cu -- radial observation kernel (World._fill_obs, engine.py:500-512;
+// fill_radial / radial_fill_core, observation.py:145-210, _fastpath.py:214-302).
 //
-// Radial mode (fill_radial / radial_fill_core, observation.py:145-210,
-// _fastpath.py:214-302): one warp per controlled agent, a CTA per world.  The
-// world's agents sit in shared memory; road points are read from the world's
-// uniform grid (device_layout.py): for every cell row that the radius disc
-// touches, the points of the covered cells form ONE contiguous, cell-sorted
-// range, read lane-strided (coalesced, L1/L2 resident across the world's
-// agents).  Distances are FP64 with the glibc hypot port (ds_math.cuh), so
-// radius membership and ordering are bit-identical to the reference.
+// Layout: one CTA per world, one warp per controlled agent (rows strided over
+// the CTA's warps).  The world's agents (FP64) and -- when they fit -- the
+// world's road points (float2 coordinates relative to the world grid origin,
+// 8 B/point) are staged once in shared memory; every warp then scans them.
+// Road candidates come from the world's uniform grid: lane l owns cell row
+// iy0 + l of the radius disc, whose covered cells form ONE contiguous,
+// cell-sorted point range.
 //
-// Exact top-k (the reference's insertion sort: nearest first, equal distances
-// keep the smaller index): candidates (d, id) are pushed into a per-warp
-// shared buffer with ballot compaction; selection is a monotone 256-bucket
-// histogram of d (prefix scan -> threshold bucket b*), a counting-sort
-// scatter of buckets <= b*, then an exact (d, id) rank inside each bucket.
-// Small sets use a direct O(n^2/32) rank.  Buffers that fill up are compacted
-// to their exact top-k on the fly (the union argument keeps this exact).
+// Exact top-k (the reference's insertion sort = ascending (distance, index)):
+//  pass 1  every candidate gets a cheap float key a ~ d^2 with a proven
+//          absolute error bound D; a 256-bucket histogram of a over
+//          [0, r^2 + D] gives the threshold bucket b* (first bucket whose
+//          cumulative count reaches k);
+//  pass 2  candidates in buckets <= b*+2 are counting-sort scattered into a
+//          small set G (about k+3 entries);
+//  exact   only G gets the glibc-exact FP64 hypot (ds_math.cuh), the exact
+//          radius test and an exact (d, id) rank.  Since |a - d^2| <= D, key
+//          order inversions only involve ADJACENT buckets and only keys within
+//          beta = 2 D / w (+ float slack) of their shared edge; such "edge"
+//          elements are ranked across the adjacent buckets, all others inside
+//          their own bucket.  Elements beyond b*+1 cannot reach rank k;
+//          out-of-radius elements can only sit in the top bucket.
+// A set G beyond its capacity (or a key bound too loose for the bucket width)
+// falls back to the reference's serial insertion -- exact by construction.
 #include "ds_internal.cuh"
 
 namespace ds {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kNB = 256;       // histogram buckets
+constexpr int kCand = 640;     // buffered pass-1 candidates (global-points variant)
+constexpr int kWarpsShared = 24;
+constexpr int kWarpsGlobal = 12;
 
-struct WarpScratch {
-  double *cd;      // [kCandCap] candidate distance
-  int *cid;        // [kCandCap] tie-break id (original index in the world)
-  int *caux;       // [kCandCap] payload (agent slot / grid-sorted point index)
-  double *sd;      // [kSelCap]
-  int *sid;
-  int *saux;
-  uint32_t *hc;    // [kBuckets] (cursor << 16) | count
-  float *row;      // [row_pad]
+__host__ __device__ inline int kmax_of(const ds_config &c) {
+  int k = c.max_agents_obs > c.max_road_points_obs ? c.max_agents_obs : c.max_road_points_obs;
+  return k < 1 ? 1 : k;
+}
+
+// Capacity of the exactly ranked set G.
+__host__ __device__ inline int gcap_of(const ds_config &c) { return kmax_of(c) + 48; }
+
+__host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
+
+// Per-warp shared scratch (byte offsets).  The observation row is staged
+// contiguously: [ego | partner slots] sit right before `hc`, and the road
+// block (11 floats per slot) aliases [hc ..), which is dead once the road
+// selection has produced sel_pl.
+struct WarpLayout {
+  size_t row, hc, ca, cp, ge, gid, gpl, gb, sel_pl, sel_id, total;
 };
 
-__host__ __device__ inline int row_pad(int obs_width) { return (obs_width + 3) & ~3; }
-
-size_t obs_smem_bytes(const ds_config &cfg, int max_agents, int warps, int obs_width) {
-  (void)cfg;
-  size_t agents = (size_t)max_agents * (6 * sizeof(double) + 1);
-  agents = (agents + 15) & ~size_t(15);
-  size_t per_warp = kCandCap * (sizeof(double) + 2 * sizeof(int)) +
-                    kSelCap * (sizeof(double) + 2 * sizeof(int)) + kBuckets * sizeof(uint32_t) +
-                    (size_t)row_pad(obs_width) * sizeof(float);
-  per_warp = (per_warp + 15) & ~size_t(15);
-  return agents + per_warp * warps;
+__host__ __device__ inline WarpLayout warp_layout(const ds_config &c, bool buffered) {
+  WarpLayout L;
+  const int km = kmax_of(c), gc = gcap_of(c);
+  const size_t head = (size_t)(7 + 7 * c.max_agents_obs) * sizeof(float);
+  size_t o = al16(head);
+  L.row = o - head;
+  L.hc = o; o = al16(o + kNB * sizeof(uint32_t));
+  L.ca = o; if (buffered) o = al16(o + kCand * sizeof(float));
+  L.cp = o; if (buffered) o = al16(o + kCand * sizeof(uint16_t));
+  L.ge = o; o = al16(o + gc * sizeof(double));
+  L.gid = o; o = al16(o + gc * sizeof(int));
+  L.gpl = o; o = al16(o + gc * sizeof(int));
+  L.gb = o; o = al16(o + gc);
+  const size_t road_end = al16(L.hc + (size_t)c.max_road_points_obs * 11 * sizeof(float));
+  if (o < road_end) o = road_end;
+  L.sel_pl = o; o = al16(o + km * sizeof(int));
+  L.sel_id = o; o = al16(o + km * sizeof(int));
+  L.total = o;
+  return L;
 }
+
+__host__ __device__ inline size_t agents_bytes(int max_agents) {
+  return al16((size_t)max_agents * (6 * sizeof(double) + 1));
+}
+
+size_t obs_smem_bytes_shared(const ds_config &cfg, int max_agents, int max_points) {
+  return agents_bytes(max_agents) + al16((size_t)max_points * sizeof(float2)) +
+         warp_layout(cfg, false).total * kWarpsShared;
+}
+
+size_t obs_smem_bytes_global(const ds_config &cfg, int max_agents) {
+  return agents_bytes(max_agents) + warp_layout(cfg, true).total * kWarpsGlobal;
+}
+
+struct Sel {
+  uint32_t *hc;
+  float *ca;
+  uint16_t *cp;
+  double *ge;
+  int *gid, *gpl;
+  uint8_t *gb;
+  int *sel_pl, *sel_id;
+  int gcap;
+};
 
 __device__ __forceinline__ bool key_less(double da, int ia, double db, int ib) {
   return da < db || (da == db && ia < ib);
 }
 
-__device__ __forceinline__ int bucket_of(double d, double scale) {
-  double b = d * scale;
-  int k = (int)b;   // d >= 0
-  return k < kBuckets ? k : kBuckets - 1;
-}
-
-// Direct rank of all n candidates: element with rank < k goes to s*[rank].
-__device__ void rank_all(const WarpScratch &ws, int n, int k, int lane) {
-  for (int p = lane; p < n; p += 32) {
-    const double dp = ws.cd[p];
-    const int ip = ws.cid[p];
-    int rank = 0;
-    for (int q = 0; q < n; ++q) rank += key_less(ws.cd[q], ws.cid[q], dp, ip) ? 1 : 0;
-    if (rank < k) {
-      ws.sd[rank] = dp;
-      ws.sid[rank] = ip;
-      ws.saux[rank] = ws.caux[p];
-    }
-  }
-}
-
-// Exact ascending top-min(n,k) of the candidate buffer, left in cd/cid/caux[0..m).
-// k <= kSelCap.  Returns m.
-__device__ int warp_topk(const WarpScratch &ws, int n, int k, double radius, int lane) {
-  const int m = n < k ? n : k;
-  if (m == 0) return 0;
-  __syncwarp();
-  if (n <= 64) {
-    rank_all(ws, n, k, lane);
-    __syncwarp();
-    for (int p = lane; p < m; p += 32) {
-      ws.cd[p] = ws.sd[p];
-      ws.cid[p] = ws.sid[p];
-      ws.caux[p] = ws.saux[p];
-    }
-    __syncwarp();
-    return m;
-  }
-  const double scale = radius > 0.0 ? (double)kBuckets / radius : 0.0;
-  for (int b = lane; b < kBuckets; b += 32) ws.hc[b] = 0u;
-  __syncwarp();
-  for (int p = lane; p < n; p += 32) atomicAdd(&ws.hc[bucket_of(ws.cd[p], scale)], 1u);
-  __syncwarp();
-  // Exclusive prefix of the counts; each lane owns 8 consecutive buckets.
-  constexpr int kPer = kBuckets / 32;
-  uint32_t cnt[kPer];
-  uint32_t local = 0;
-#pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    cnt[q] = ws.hc[lane * kPer + q];
-    local += cnt[q];
-  }
-  uint32_t incl = local;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t up = __shfl_up_sync(kFull, incl, off);
-    if (lane >= off) incl += up;
-  }
-  uint32_t run = incl - local;
-  // Threshold bucket b*: first bucket whose inclusive count reaches k.
-  int bstar = kBuckets;
-#pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    ws.hc[lane * kPer + q] = (run << 16) | cnt[q];
-    if (bstar == kBuckets && run < (uint32_t)k && run + cnt[q] >= (uint32_t)k) bstar = lane * kPer + q;
-    run += cnt[q];
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) bstar = min(bstar, __shfl_xor_sync(kFull, bstar, off));
-  const uint32_t n_sel = bstar < kBuckets ? ((ws.hc[bstar] >> 16) + (ws.hc[bstar] & 0xffffu))
-                                          : (uint32_t)n;
-  __syncwarp();
-  if (n_sel > (uint32_t)kSelCap) {
-    // Pathological threshold bucket: exact O(n^2) rank of everything.
-    rank_all(ws, n, k, lane);
-    __syncwarp();
-    for (int p = lane; p < m; p += 32) {
-      ws.cd[p] = ws.sd[p];
-      ws.cid[p] = ws.sid[p];
-      ws.caux[p] = ws.saux[p];
-    }
-    __syncwarp();
-    return m;
-  }
-  // Counting-sort scatter of buckets <= b*.
-  for (int p = lane; p < n; p += 32) {
-    const int b = bucket_of(ws.cd[p], scale);
-    if (b <= bstar) {
-      const uint32_t pos = atomicAdd(&ws.hc[b], 1u << 16) >> 16;
-      ws.sd[pos] = ws.cd[p];
-      ws.sid[pos] = ws.cid[p];
-      ws.saux[pos] = ws.caux[p];
-    }
-  }
-  __syncwarp();
-  // Exact (d, id) rank inside each bucket; cursor now = start + count.
-  for (int p = lane; p < (int)n_sel; p += 32) {
-    const double dp = ws.sd[p];
-    const int ip = ws.sid[p];
-    const uint32_t hcv = ws.hc[bucket_of(dp, scale)];
-    const int cntb = (int)(hcv & 0xffffu);
-    const int start = (int)(hcv >> 16) - cntb;
-    int rank = start;
-    for (int q = start; q < start + cntb; ++q) rank += key_less(ws.sd[q], ws.sid[q], dp, ip) ? 1 : 0;
-    if (rank < k) {
-      ws.cd[rank] = dp;
-      ws.cid[rank] = ip;
-      ws.caux[rank] = ws.saux[p];
-    }
-  }
-  __syncwarp();
-  return m;
-}
-
-// Ballot-compacted push of one candidate per lane into the buffer.
-__device__ __forceinline__ int warp_push(const WarpScratch &ws, int n, bool ok, double d, int id,
-                                         int aux, int lane) {
-  const unsigned bal = __ballot_sync(kFull, ok);
-  if (ok) {
-    const int pos = n + __popc(bal & ((1u << lane) - 1u));
-    ws.cd[pos] = d;
-    ws.cid[pos] = id;
-    ws.caux[pos] = aux;
-  }
-  return n + __popc(bal);
+__device__ __forceinline__ int bucket_of(float a, float inv_w) {
+  const int b = (int)(a * inv_w);
+  return b < kNB ? b : kNB - 1;
 }
 
 __device__ __forceinline__ int clampi(double f, int lo, int hi) {
@@ -183,11 +113,350 @@ __device__ __forceinline__ int clampi(double f, int lo, int hi) {
   return (int)f;
 }
 
-template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) obs_radial_kernel(ds_tables T, ds_config C,
-                                                              ds_state S, const uint8_t *mask,
-                                                              float *obs, const float *scale,
-                                                              int32_t *sel_idx, int obs_width) {
+// Cell rows of a query disc around (px, py): lane l owns row iy0 + l; the
+// covered cells of a row are one contiguous range of the cell-sorted points.
+struct RowGeo {
+  const int *cell_start;   // world's cell CSR (absolute point indices)
+  double px, py, gx0, gy0, cs, inv_cs;
+  int nx, ny, iy0, nrows;
+  __device__ __forceinline__ void init(double reach) {
+    const double fy0 = (py - reach - gy0) * inv_cs, fy1 = (py + reach - gy0) * inv_cs;
+    iy0 = 0;
+    nrows = 0;
+    if (nx > 0 && ny > 0 && fy1 >= 0.0 && fy0 < (double)ny) {
+      iy0 = clampi(floor(fy0), 0, ny - 1);
+      nrows = clampi(floor(fy1), 0, ny - 1) - iy0 + 1;
+      nrows = nrows < 32 ? nrows : 32;
+    }
+  }
+  // range of lane's row for radius `reach` (a superset of the disc's points)
+  __device__ __forceinline__ void range(double reach, int lane, int &sb, int &cnt) const {
+    sb = 0;
+    cnt = 0;
+    if (lane >= nrows) return;
+    const int iy = iy0 + lane;
+    const double ylo = gy0 + iy * cs, yhi = ylo + cs;
+    double dyb = 0.0;
+    if (py < ylo) dyb = ylo - py;
+    else if (py > yhi) dyb = py - yhi;
+    if (dyb > reach) return;
+    const double half = sqrt(reach * reach - dyb * dyb) + 1e-6;
+    const double fx0 = (px - half - gx0) * inv_cs, fx1 = (px + half - gx0) * inv_cs;
+    if (fx1 < 0.0 || fx0 >= (double)nx) return;
+    const int ix0 = clampi(floor(fx0), 0, nx - 1), ix1 = clampi(floor(fx1), 0, nx - 1);
+    const int *c = cell_start + (int64_t)iy * nx;
+    sb = c[ix0];
+    cnt = c[ix1 + 1] - sb;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Candidate sources.  visit(r2hi, lane, fn) calls fn(ok, key, payload)
+// warp-collectively, one candidate per lane; exact(payload, id) returns the
+// reference's distance (glibc hypot port) and the tie-break index.
+// ---------------------------------------------------------------------------
+
+// Agents of the world (partner slots, fp:240-272), FP64 in shared memory.
+// Key: fl32 of an FP64 d^2 -> |a - d^2| <= 2^-22 r2hi.
+struct PartnerSrc {
+  const double *x, *y;
+  const uint8_t *vis;
+  int n, self;
+  double px, py;
+  __device__ __forceinline__ int pbase() const { return 0; }
+  __device__ __forceinline__ bool small_payload() const { return true; }
+  template <class F>
+  __device__ __forceinline__ void visit(float r2hi, int lane, F &&fn) const {
+    for (int f0 = 0; f0 < n; f0 += 32) {
+      const int f = f0 + lane;
+      bool ok = f < n && f != self && vis[f];
+      float a = 0.0f;
+      if (ok) {
+        const double dx = x[f] - px, dy = y[f] - py;
+        a = (float)fma(dx, dx, dy * dy);
+        ok = a <= r2hi;
+      }
+      fn(ok, a, f);
+    }
+  }
+  __device__ __forceinline__ double exact(int pl, int &id) const {
+    id = pl;
+    return hypot(x[pl] - px, y[pl] - py);
+  }
+  __device__ __forceinline__ void restrict_to(double, int) {}
+};
+
+// Road points staged in shared memory as float2 relative to the grid origin.
+// dx = fl32(xr - pr) with |xr - (x - x0)| <= eps_p (host-measured) and
+// |pr - (px - x0)| measured per agent: see the bound D in the kernel.
+struct RoadSrcShared {
+  const float2 *pts;                 // shared, world-relative index
+  const double *__restrict__ gx, *__restrict__ gy;
+  const int *__restrict__ gid;
+  int sb, cnt, nrows, p0;            // sb relative to p0
+  float prx, pry;
+  double px, py;
+  const RowGeo *geo;
+  // shrink the scanned rows to the disc of radius rho (pass 2)
+  __device__ __forceinline__ void restrict_to(double rho, int lane) {
+    int b, c;
+    geo->range(rho, lane, b, c);
+    sb = b - p0;
+    cnt = c;
+  }
+  __device__ __forceinline__ int pbase() const { return 0; }
+  __device__ __forceinline__ bool small_payload() const { return true; }
+  template <class F>
+  __device__ __forceinline__ void visit(float r2hi, int lane, F &&fn) const {
+    for (int r = 0; r < nrows; ++r) {
+      const int rb = __shfl_sync(kFull, sb, r);
+      const int rc = __shfl_sync(kFull, cnt, r);
+      for (int j0 = 0; j0 < rc; j0 += 32) {
+        const int j = j0 + lane;
+        bool ok = j < rc;
+        float a = 0.0f;
+        if (ok) {
+          const float2 p = pts[rb + j];
+          const float dx = p.x - prx, dy = p.y - pry;
+          a = fmaf(dx, dx, dy * dy);
+          ok = a <= r2hi;
+        }
+        fn(ok, a, rb + j);
+      }
+    }
+  }
+  __device__ __forceinline__ double exact(int pl, int &id) const {
+    id = gid[p0 + pl];
+    return hypot(gx[p0 + pl] - px, gy[p0 + pl] - py);
+  }
+};
+
+// Road points read from global memory (worlds too large for shared memory).
+struct RoadSrcGlobal {
+  const double *__restrict__ gx, *__restrict__ gy;
+  const int *__restrict__ gid;
+  int sb, cnt, nrows, p0, np;        // sb absolute
+  double px, py;
+  const RowGeo *geo;
+  __device__ __forceinline__ void restrict_to(double rho, int lane) { geo->range(rho, lane, sb, cnt); }
+  __device__ __forceinline__ int pbase() const { return p0; }
+  __device__ __forceinline__ bool small_payload() const { return np <= 0xffff; }
+  template <class F>
+  __device__ __forceinline__ void visit(float r2hi, int lane, F &&fn) const {
+    for (int r = 0; r < nrows; ++r) {
+      const int rb = __shfl_sync(kFull, sb, r);
+      const int rc = __shfl_sync(kFull, cnt, r);
+      for (int j0 = 0; j0 < rc; j0 += 32) {
+        const int j = j0 + lane;
+        bool ok = j < rc;
+        float a = 0.0f;
+        if (ok) {
+          const double dx = gx[rb + j] - px, dy = gy[rb + j] - py;
+          a = (float)fma(dx, dx, dy * dy);
+          ok = a <= r2hi;
+        }
+        fn(ok, a, rb + j);
+      }
+    }
+  }
+  __device__ __forceinline__ double exact(int pl, int &id) const {
+    id = gid[pl];
+    return hypot(gx[pl] - px, gy[pl] - py);
+  }
+};
+
+// Serial exact insertion (the reference's algorithm): the fallback.
+template <class Src>
+__device__ int select_serial(const Src &src, int k, double radius, float r2hi, const Sel &S,
+                             int lane) {
+  int cnt = 0;
+  src.visit(r2hi, lane, [&](bool ok, float, int pl) {
+    int id = 0;
+    double e = 0.0;
+    if (ok) {
+      e = src.exact(pl, id);
+      ok = e <= radius;
+    }
+    unsigned bal = __ballot_sync(kFull, ok);
+    while (bal) {
+      const int src_lane = __ffs(bal) - 1;
+      bal &= bal - 1;
+      const double ej = __shfl_sync(kFull, e, src_lane);
+      const int idj = __shfl_sync(kFull, id, src_lane);
+      const int plj = __shfl_sync(kFull, pl, src_lane);
+      if (lane == 0) {
+        int m;
+        bool take = true;
+        if (cnt < k) {
+          m = cnt++;
+        } else if (key_less(ej, idj, S.ge[k - 1], S.gid[k - 1])) {
+          m = k - 1;
+        } else {
+          take = false;
+          m = 0;
+        }
+        if (take) {
+          while (m > 0 && key_less(ej, idj, S.ge[m - 1], S.gid[m - 1])) {
+            S.ge[m] = S.ge[m - 1];
+            S.gid[m] = S.gid[m - 1];
+            S.gpl[m] = S.gpl[m - 1];
+            --m;
+          }
+          S.ge[m] = ej;
+          S.gid[m] = idj;
+          S.gpl[m] = plj;
+        }
+      }
+      __syncwarp();
+    }
+  });
+  cnt = __shfl_sync(kFull, cnt, 0);
+  for (int m = lane; m < cnt; m += 32) {
+    S.sel_pl[m] = S.gpl[m];
+    S.sel_id[m] = S.gid[m];
+  }
+  __syncwarp();
+  return cnt;
+}
+
+// Exact ascending top-min(n_valid, k) by (distance, id) given candidate keys
+// with |a - d^2| <= D.  Payloads land in S.sel_pl[0..m), ids in S.sel_id.
+// Warp-collective.  Buffered: pass 1 keeps (key, payload) in shared memory.
+template <bool Buffered, class Src>
+__device__ int select_topk(Src src, int k, double radius, double D, const Sel &S, int lane) {
+  if (k <= 0) return 0;
+  const double r2 = radius * radius;
+  const float r2hi = (float)((r2 + D) * (1.0 + 1e-7) + 1e-30);
+  const float inv_w = r2hi > 0.0f ? (float)kNB / r2hi : 0.0f;
+  // edge band in bucket units: twice the key error plus float slack
+  const float beta = (float)(2.0 * D * (double)inv_w) + 4e-5f;
+  if (!(beta < 0.125f)) return select_serial(src, k, radius, r2hi, S, lane);
+  for (int b = lane; b < kNB; b += 32) S.hc[b] = 0u;
+  __syncwarp();
+  const int pb = src.pbase();
+  int nbuf = 0;
+  src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
+    if (ok) atomicAdd(&S.hc[bucket_of(a, inv_w)], 1u);
+    if (Buffered) {
+      const unsigned bal = __ballot_sync(kFull, ok);
+      const int pos = nbuf + __popc(bal & ((1u << lane) - 1u));
+      if (ok && pos < kCand) {
+        S.ca[pos] = a;
+        S.cp[pos] = (uint16_t)(pl - pb);
+      }
+      nbuf += __popc(bal);
+    }
+  });
+  __syncwarp();
+  constexpr int kPer = kNB / 32;
+  uint32_t cnt[kPer];
+  uint32_t local = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    cnt[q] = S.hc[lane * kPer + q];
+    local += cnt[q];
+  }
+  uint32_t incl = local;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t up = __shfl_up_sync(kFull, incl, off);
+    if (lane >= off) incl += up;
+  }
+  const uint32_t total = __shfl_sync(kFull, incl, 31);
+  if (total == 0) return 0;
+  uint32_t run = incl - local;
+  int bstar = kNB - 1;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    if (run < (uint32_t)k && run + cnt[q] >= (uint32_t)k) bstar = lane * kPer + q;
+    run += cnt[q];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) bstar = min(bstar, __shfl_xor_sync(kFull, bstar, off));
+  const int bmax = min(bstar + 2, kNB - 1);
+  uint32_t run2 = incl - local, n_g = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int b = lane * kPer + q;
+    S.hc[b] = (run2 << 16) | cnt[q];
+    run2 += cnt[q];
+    if (b == bmax) n_g = run2;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) n_g = max(n_g, __shfl_xor_sync(kFull, n_g, off));
+  __syncwarp();
+  if (n_g > (uint32_t)S.gcap || total > 0xffffu)
+    return select_serial(src, k, radius, r2hi, S, lane);
+  // pass 2: counting-sort scatter of buckets <= bmax into G
+  auto scatter = [&](float a, int pl) {
+    const int b = bucket_of(a, inv_w);
+    if (b <= bmax) {
+      const uint32_t pos = atomicAdd(&S.hc[b], 1u << 16) >> 16;
+      S.gpl[pos] = pl;
+      S.gb[pos] = (uint8_t)b;
+      S.ge[pos] = (double)a;   // key parked for the edge test
+    }
+  };
+  if (Buffered && nbuf <= kCand && src.small_payload()) {
+    for (int p = lane; p < nbuf; p += 32) scatter(S.ca[p], pb + (int)S.cp[p]);
+  } else {
+    // only keys in buckets <= bmax matter: a < (bmax + 1) w, so d^2 < that + D
+    if (bmax < kNB - 1) src.restrict_to(sqrt(((double)bmax + 1.001) / (double)inv_w + D) + 1e-6, lane);
+    src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
+      if (ok) scatter(a, pl);
+    });
+  }
+  __syncwarp();
+  // exact keys for G; out-of-radius -> +inf (never counted, never selected);
+  // the edge flag rides in the payload's complement until ranking
+  int n_valid = 0;
+  for (int p = lane; p < (int)n_g; p += 32) {
+    const float t = (float)S.ge[p] * inv_w;
+    const float fr = t - floorf(t);
+    const bool edge = fr < beta || fr > 1.0f - beta;
+    int id;
+    const int pl = S.gpl[p];
+    const double e = src.exact(pl, id);
+    const bool v = e <= radius;
+    S.ge[p] = v ? e : INFINITY;
+    S.gid[p] = id;
+    if (edge) S.gpl[p] = ~pl;
+    n_valid += v;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) n_valid += __shfl_xor_sync(kFull, n_valid, off);
+  __syncwarp();
+  // exact rank: own bucket, or across the adjacent buckets for edge elements
+  for (int p = lane; p < (int)n_g; p += 32) {
+    const double ep = S.ge[p];
+    if (ep == INFINITY) continue;
+    const int plp = S.gpl[p];
+    const bool edge = plp < 0;
+    const int ip = S.gid[p];
+    const int b = S.gb[p];
+    const int lo = edge ? (b > 0 ? b - 1 : 0) : b;
+    const int hi = edge ? (b < bmax ? b + 1 : bmax) : b;
+    const uint32_t hlo = S.hc[lo], hhi = S.hc[hi];
+    const int start = (int)(hlo >> 16) - (int)(hlo & 0xffffu);
+    const int end = (int)(hhi >> 16);
+    int rank = start;
+    for (int q = start; q < end; ++q) rank += key_less(S.ge[q], S.gid[q], ep, ip) ? 1 : 0;
+    if (rank < k) {
+      S.sel_pl[rank] = edge ? ~plp : plp;
+      S.sel_id[rank] = ip;
+    }
+  }
+  __syncwarp();
+  return n_valid < k ? n_valid : k;
+}
+
+// ---------------------------------------------------------------------------
+// The kernel.  SharedPts: road points staged in shared memory (float2).
+// ---------------------------------------------------------------------------
+template <int WARPS, bool SharedPts>
+__global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kernel(
+    ds_tables T, ds_config C, ds_state St, const uint8_t *mask, float *obs, const float *scale,
+    int32_t *sel_idx, int obs_width) {
   const int w = blockIdx.x;
   if (mask && !mask[w]) return;
   const int64_t c0 = T.c_off[w];
@@ -199,36 +468,43 @@ __global__ void __launch_bounds__(WARPS * 32) obs_radial_kernel(ds_tables T, ds_
   double *ay = ax + amax, *ah = ax + 2 * amax, *av = ax + 3 * amax, *al = ax + 4 * amax,
          *aw = ax + 5 * amax;
   uint8_t *avis = reinterpret_cast<uint8_t *>(ax + 6 * amax);
-  size_t agents_bytes = ((size_t)amax * (6 * sizeof(double) + 1) + 15) & ~size_t(15);
-  const int rp = row_pad(obs_width);
-  size_t per_warp = kCandCap * (sizeof(double) + 2 * sizeof(int)) +
-                    kSelCap * (sizeof(double) + 2 * sizeof(int)) + kBuckets * sizeof(uint32_t) +
-                    (size_t)rp * sizeof(float);
-  per_warp = (per_warp + 15) & ~size_t(15);
+  unsigned char *after_agents = smem_raw + agents_bytes(amax);
+  const int64_t p0 = T.p_off[w];
+  const int np = (int)(T.p_off[w + 1] - p0);
+  float2 *pts = reinterpret_cast<float2 *>(after_agents);
+  const WarpLayout WL = warp_layout(C, !SharedPts);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char *wb = smem_raw + agents_bytes + per_warp * warp;
-  WarpScratch ws;
-  ws.cd = reinterpret_cast<double *>(wb);
-  ws.sd = ws.cd + kCandCap;
-  ws.cid = reinterpret_cast<int *>(ws.sd + kSelCap);
-  ws.caux = ws.cid + kCandCap;
-  ws.sid = ws.caux + kCandCap;
-  ws.saux = ws.sid + kSelCap;
-  ws.hc = reinterpret_cast<uint32_t *>(ws.saux + kSelCap);
-  ws.row = reinterpret_cast<float *>(ws.hc + kBuckets);
+  unsigned char *wb = after_agents + (SharedPts ? al16((size_t)T.max_points * sizeof(float2)) : 0) +
+                      WL.total * warp;
+  Sel S;
+  S.hc = reinterpret_cast<uint32_t *>(wb + WL.hc);
+  S.ca = reinterpret_cast<float *>(wb + WL.ca);
+  S.cp = reinterpret_cast<uint16_t *>(wb + WL.cp);
+  S.ge = reinterpret_cast<double *>(wb + WL.ge);
+  S.gid = reinterpret_cast<int *>(wb + WL.gid);
+  S.gpl = reinterpret_cast<int *>(wb + WL.gpl);
+  S.gb = wb + WL.gb;
+  S.sel_pl = reinterpret_cast<int *>(wb + WL.sel_pl);
+  S.sel_id = reinterpret_cast<int *>(wb + WL.sel_id);
+  S.gcap = gcap_of(C);
+  float *row = reinterpret_cast<float *>(wb + WL.row);   // contiguous staged row
 
   const int64_t a0 = T.a_off[w];
   const int A = (int)(T.a_off[w + 1] - a0);
   for (int i = threadIdx.x; i < A; i += blockDim.x) {
     const int64_t g = a0 + i;
-    ax[i] = S.x[g];
-    ay[i] = S.y[g];
-    ah[i] = S.heading[g];
-    av[i] = S.speed[g];
+    ax[i] = St.x[g];
+    ay[i] = St.y[g];
+    ah[i] = St.heading[g];
+    av[i] = St.speed[g];
     al[i] = T.length[g];
     aw[i] = T.width[g];
-    const uint16_t f = S.flags[g];
+    const uint16_t f = St.flags[g];
     avis[i] = (f & DS_F_PRESENT) && !(f & DS_F_REMOVED);
+  }
+  if (SharedPts) {
+    const float2 *src = reinterpret_cast<const float2 *>(T.gpt_xy) + p0;
+    for (int j = threadIdx.x; j < np; j += blockDim.x) pts[j] = src[j];
   }
   __syncthreads();
 
@@ -239,15 +515,17 @@ __global__ void __launch_bounds__(WARPS * 32) obs_radial_kernel(ds_tables T, ds_
   const int sel_w = cap_a + cap_r;
   const int nx = T.grid_nx[w], ny = T.grid_ny[w];
   const double gx0 = T.grid_x0[w], gy0 = T.grid_y0[w], cs = C.grid_cell;
+  const double inv_cs = 1.0 / cs;
   const int64_t cbase = T.grid_cell_off[w];
-  const int64_t p0 = T.p_off[w];
+  const double eps_p = SharedPts ? T.grid_eps[w] : 0.0;
+  const double D_fp64 = (radius * radius + 1.0) * 2.4e-7;   // fl32 of an FP64 d^2
 
   for (int r = warp; r < nrow; r += WARPS) {
     const int64_t orow = c0 + r;
     float *out = obs + orow * (int64_t)obs_width;
     const int64_t g = T.row_agent[orow];
     const int i = (int)(g - a0);
-    const uint16_t f = S.flags[g];
+    const uint16_t f = St.flags[g];
     if (f & (DS_F_DONE | DS_F_REMOVED)) {
       // finished / removed rows are zero-filled (engine.py:502-512)
       for (int c = lane; c < obs_width; c += 32) out[c] = 0.0f;
@@ -255,40 +533,28 @@ __global__ void __launch_bounds__(WARPS * 32) obs_radial_kernel(ds_tables T, ds_
         for (int c = lane; c < sel_w; c += 32) sel_idx[orow * sel_w + c] = -1;
       continue;
     }
-    for (int c = lane; c < rp; c += 32) ws.row[c] = 0.0f;
     const double px = ax[i], py = ay[i], h = ah[i];
     const double ch = cos(h), sh = sin(h);
-    __syncwarp();
     if (lane == 0) {
       // ego block (fp:228-238)
       const double gx = T.goal_x[g] - px, gy = T.goal_y[g] - py;
-      ws.row[0] = (float)av[i];
-      ws.row[1] = (float)al[i];
-      ws.row[2] = (float)aw[i];
-      ws.row[3] = (float)(gx * ch + gy * sh);
-      ws.row[4] = (float)(gy * ch - gx * sh);
-      ws.row[5] = (float)hypot(gx, gy);
-      ws.row[6] = (f & DS_F_COLLIDED) ? 1.0f : 0.0f;
+      row[0] = (float)av[i];
+      row[1] = (float)al[i];
+      row[2] = (float)aw[i];
+      row[3] = (float)(gx * ch + gy * sh);
+      row[4] = (float)(gy * ch - gx * sh);
+      row[5] = (float)hypot(gx, gy);
+      row[6] = (f & DS_F_COLLIDED) ? 1.0f : 0.0f;
     }
 
-    // ---- partners: visible, j != i, hypot <= radius, k nearest (fp:240-272)
-    int n = 0;
-    for (int j0 = 0; j0 < A; j0 += 32) {
-      const int j = j0 + lane;
-      bool ok = j < A && j != i && avis[j];
-      double d = 0.0;
-      if (ok) {
-        d = hypot(ax[j] - px, ay[j] - py);
-        ok = d <= radius;
-      }
-      n = warp_push(ws, n, ok, d, j, j, lane);
-      if (n > kCandCap - 32) n = warp_topk(ws, n, cap_a, radius, lane);
-    }
-    const int ma = warp_topk(ws, n, cap_a, radius, lane);
+    // ---- partners
+    PartnerSrc psrc{ax, ay, avis, A, i, px, py};
+    const int ma = select_topk<false>(psrc, cap_a, radius, D_fp64, S, lane);
+    float *ps = row + 7;
     for (int m = lane; m < ma; m += 32) {
-      const int j = ws.cid[m];
+      const int j = S.sel_pl[m];
       const double dx = ax[j] - px, dy = ay[j] - py;
-      float *slot = ws.row + 7 + 7 * m;
+      float *slot = ps + 7 * m;
       slot[0] = (float)(dx * ch + dy * sh);
       slot[1] = (float)(dy * ch - dx * sh);
       slot[2] = (float)wrap(ah[j] - h);
@@ -298,91 +564,101 @@ __global__ void __launch_bounds__(WARPS * 32) obs_radial_kernel(ds_tables T, ds_
       slot[6] = 1.0f;
       if (sel_idx) sel_idx[orow * sel_w + m] = j;
     }
+    for (int q = 7 * ma + lane; q < 7 * cap_a; q += 32) ps[q] = 0.0f;
     if (sel_idx)
       for (int m = ma + lane; m < cap_a; m += 32) sel_idx[orow * sel_w + m] = -1;
     __syncwarp();
 
-    // ---- road points within the radius, k nearest (fp:274-302)
-    n = 0;
-    if (cap_r > 0 && nx > 0 && ny > 0) {
-      const double fy0 = (py - reach - gy0) / cs, fy1 = (py + reach - gy0) / cs;
-      if (fy1 >= 0.0 && fy0 < (double)ny) {
-        const int iy0 = clampi(floor(fy0), 0, ny - 1), iy1 = clampi(floor(fy1), 0, ny - 1);
-        for (int iy = iy0; iy <= iy1; ++iy) {
-          const double ylo = gy0 + iy * cs, yhi = ylo + cs;
-          double dyb = 0.0;
-          if (py < ylo) dyb = ylo - py;
-          else if (py > yhi) dyb = py - yhi;
-          if (dyb > reach) continue;
-          const double half = sqrt(reach * reach - dyb * dyb) + 1e-6;
-          const double fx0 = (px - half - gx0) / cs, fx1 = (px + half - gx0) / cs;
-          if (fx1 < 0.0 || fx0 >= (double)nx) continue;
-          const int ix0 = clampi(floor(fx0), 0, nx - 1), ix1 = clampi(floor(fx1), 0, nx - 1);
-          const int64_t cell = cbase + (int64_t)iy * nx;
-          const int sb = T.pt_cell_start[cell + ix0], se = T.pt_cell_start[cell + ix1 + 1];
-          for (int s0 = sb; s0 < se; s0 += 32) {
-            const int s = s0 + lane;
-            bool ok = s < se;
-            double d = 0.0;
-            int id = 0;
-            if (ok) {
-              const double dx = T.gpt_x[s] - px, dy = T.gpt_y[s] - py;
-              ok = fabs(dx) <= reach && fabs(dy) <= reach;
-              if (ok) {
-                d = hypot(dx, dy);
-                ok = d <= radius;
-                id = T.gpt_id[s];
-              }
-            }
-            n = warp_push(ws, n, ok, d, id, s, lane);
-            if (n > kCandCap - 32) n = warp_topk(ws, n, cap_r, radius, lane);
-          }
-        }
+    // ---- road points: lane l owns cell row iy0 + l of the disc
+    int mr = 0;
+    if (cap_r > 0) {
+      RowGeo geo{T.pt_cell_start + cbase, px, py, gx0, gy0, cs, inv_cs, nx, ny, 0, 0};
+      geo.init(reach);
+      int sb, cnt;
+      geo.range(reach, lane, sb, cnt);
+      if (SharedPts) {
+        const double rx = px - gx0, ry = py - gy0;
+        const float prx = (float)rx, pry = (float)ry;
+        // key bound: |dx_f - dx| <= E; |a - d^2| <= 4 (r + 1) E + 2 E^2 + fl32 rounding
+        const double E = eps_p + fmax(fabs((double)prx - rx), fabs((double)pry - ry)) +
+                         (radius + 1.0) * 1.2e-7;
+        const double D = 4.0 * (radius + 1.0) * E + 2.0 * E * E + D_fp64;
+        RoadSrcShared rsrc{pts, T.gpt_x, T.gpt_y, T.gpt_id, sb - (int)p0, cnt, geo.nrows, (int)p0,
+                           prx, pry, px, py, &geo};
+        mr = select_topk<false>(rsrc, cap_r, radius, D, S, lane);
+      } else {
+        RoadSrcGlobal rsrc{T.gpt_x, T.gpt_y, T.gpt_id, sb, cnt, geo.nrows, (int)p0, np, px, py, &geo};
+        mr = select_topk<true>(rsrc, cap_r, radius, D_fp64, S, lane);
       }
     }
-    const int mr = warp_topk(ws, n, cap_r, radius, lane);
-    for (int m = lane; m < mr; m += 32) {
-      const int s = ws.caux[m];
-      const double dx = T.gpt_x[s] - px, dy = T.gpt_y[s] - py;
-      float *slot = ws.row + road_off + 11 * m;
-      slot[0] = (float)(dx * ch + dy * sh);
-      slot[1] = (float)(dy * ch - dx * sh);
-      slot[2] = (float)wrap(T.gpt_h[s] - h);
-      slot[3 + T.gpt_kind[s]] = 1.0f;
-      slot[10] = 1.0f;
-      if (sel_idx) sel_idx[orow * sel_w + cap_a + m] = ws.cid[m];
+    // road block staged as the final 11-float slots (aliases the dead scratch)
+    float *rstage = row + road_off;
+    const int sel_off = SharedPts ? (int)p0 : 0;
+    for (int m = lane; m < cap_r; m += 32) {
+      float *slot = rstage + 11 * m;
+      if (m < mr) {
+        const int s = S.sel_pl[m] + sel_off;
+        const double dx = T.gpt_x[s] - px, dy = T.gpt_y[s] - py;
+        const int kind = T.gpt_kind[s];
+        slot[0] = (float)(dx * ch + dy * sh);
+        slot[1] = (float)(dy * ch - dx * sh);
+        slot[2] = (float)wrap(T.gpt_h[s] - h);
+#pragma unroll
+        for (int q = 0; q < 7; ++q) slot[3 + q] = q == kind ? 1.0f : 0.0f;
+        slot[10] = 1.0f;
+        if (sel_idx) sel_idx[orow * sel_w + cap_a + m] = S.sel_id[m];
+      } else {
+#pragma unroll
+        for (int q = 0; q < 11; ++q) slot[q] = 0.0f;
+        if (sel_idx) sel_idx[orow * sel_w + cap_a + m] = -1;
+      }
     }
-    if (sel_idx)
-      for (int m = mr + lane; m < cap_r; m += 32) sel_idx[orow * sel_w + cap_a + m] = -1;
     __syncwarp();
+    // ---- coalesced write-out of the staged row
     if (scale) {
-      for (int c = lane; c < obs_width; c += 32) out[c] = ws.row[c] / scale[c];
+      for (int c = lane; c < obs_width; c += 32) out[c] = row[c] / scale[c];
     } else {
-      for (int c = lane; c < obs_width; c += 32) out[c] = ws.row[c];
+      for (int c = lane; c < obs_width; c += 32) out[c] = row[c];
     }
     __syncwarp();
   }
-  (void)p0;
 }
 
-constexpr int kObsWarps = 8;
-
 cudaError_t configure_kernels(int max_dynamic_smem) {
-  cudaError_t e = cudaFuncSetAttribute(obs_radial_kernel<kObsWarps>,
+  cudaError_t e = cudaFuncSetAttribute(obs_radial_kernel<kWarpsShared, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        max_dynamic_smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(obs_radial_kernel<kWarpsGlobal, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, max_dynamic_smem);
   if (e != cudaSuccess) return e;
   return configure_step_kernels(max_dynamic_smem);
 }
 
+void obs_plan(ds_handle *h, int max_optin) {
+  const size_t sh = obs_smem_bytes_shared(h->cfg, h->tab.max_agents, h->tab.max_points);
+  if (h->tab.gpt_xy && h->tab.grid_eps && sh <= (size_t)max_optin) {
+    h->obs_shared_pts = 1;
+    h->obs_warps = kWarpsShared;
+    h->obs_smem = sh;
+  } else {
+    h->obs_shared_pts = 0;
+    h->obs_warps = kWarpsGlobal;
+    h->obs_smem = obs_smem_bytes_global(h->cfg, h->tab.max_agents);
+  }
+}
+
 cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, float *obs,
                            const float *scale, int32_t *sel_idx, cudaStream_t s) {
-  if (h->cfg.obs_mode == DS_OBS_RADIAL) {
-    obs_radial_kernel<kObsWarps><<<h->tab.n_worlds, kObsWarps * 32, h->obs_smem, s>>>(
+  if (h->cfg.obs_mode != DS_OBS_RADIAL) return cudaErrorNotSupported;
+  if (h->obs_shared_pts) {
+    obs_radial_kernel<kWarpsShared, true><<<h->tab.n_worlds, kWarpsShared * 32, h->obs_smem, s>>>(
         h->tab, h->cfg, h->st, mask, obs, scale, sel_idx, h->obs_width);
-    return cudaGetLastError();
+  } else {
+    obs_radial_kernel<kWarpsGlobal, false><<<h->tab.n_worlds, kWarpsGlobal * 32, h->obs_smem, s>>>(
+        h->tab, h->cfg, h->st, mask, obs, scale, sel_idx, h->obs_width);
   }
-  return cudaErrorNotSupported;
+  return cudaGetLastError();
 }
 
 }  // namespace ds

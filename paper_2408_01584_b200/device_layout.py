@@ -51,6 +51,8 @@ class DeviceLayout:
     aseg_by: np.ndarray
     aseg_id: np.ndarray
     aseg_edge: np.ndarray
+    gpt_xy: np.ndarray        # f32 [P, 2] grid-sorted, relative to (grid_x0, grid_y0)
+    grid_eps: np.ndarray      # f64 [W] max |f32 - exact| of those coordinates
 
 
 def _bin_segments(pw: PackedWorlds, sel: np.ndarray, world_of_seg: np.ndarray,
@@ -147,6 +149,17 @@ def build_layout(pw: PackedWorlds, cell: float = 8.0, all_segments: bool = True)
     as_, aorder = _bin_segments(pw, np.full(len(world_of_seg), bool(all_segments)), world_of_seg,
                                 x0, y0, nx, ny, cell_base, n_cells_total, cell)
     seg_local = np.arange(len(world_of_seg)) - np.repeat(pw.s_off[:-1], S)
+    # float2 coordinates relative to the world origin for the shared-memory scan,
+    # with the exact per-world rounding bound used by the key error analysis
+    ws = world_of_pt[order] if len(order) else np.zeros(0, np.int64)
+    relx = pw.pt_x[order] - x0[ws]
+    rely = pw.pt_y[order] - y0[ws]
+    gxy = np.stack([relx, rely], -1).astype(np.float32)
+    err = np.maximum(np.abs(gxy[:, 0].astype(np.float64) - relx),
+                     np.abs(gxy[:, 1].astype(np.float64) - rely)) if len(ws) else np.zeros(0)
+    eps = np.zeros(W)
+    if len(ws):
+        np.maximum.at(eps, ws, err)
     return DeviceLayout(
         cell=float(cell), grid_x0=x0.astype(np.float64), grid_y0=y0.astype(np.float64),
         grid_nx=nx.astype(np.int32), grid_ny=ny.astype(np.int32), grid_cell_off=cell_base_ptr,
@@ -157,4 +170,5 @@ def build_layout(pw: PackedWorlds, cell: float = 8.0, all_segments: bool = True)
         eseg_bx=pw.seg_bx[eorder], eseg_by=pw.seg_by[eorder],
         aseg_cell_start=per_world_ptr(as_), aseg_ax=pw.seg_ax[aorder], aseg_ay=pw.seg_ay[aorder],
         aseg_bx=pw.seg_bx[aorder], aseg_by=pw.seg_by[aorder],
-        aseg_id=seg_local[aorder].astype(np.int32), aseg_edge=edge[aorder].astype(np.uint8))
+        aseg_id=seg_local[aorder].astype(np.int32), aseg_edge=edge[aorder].astype(np.uint8),
+        gpt_xy=np.ascontiguousarray(gxy), grid_eps=eps)

@@ -134,8 +134,11 @@ def make_native_config(cfg: SimConfig, grid_cell: float) -> N.DsConfig:
 
 
 def default_grid_cell(obs: ObsConfig) -> float:
-    """Cell edge of the static road grid: ~radius/6 for radial queries."""
-    return 8.0 if obs.mode == "radial" else 10.0
+    """Cell edge of the static road grid (8 m; a radial query disc must span
+    at most 32 cell rows, one per lane)."""
+    if obs.mode == "radial":
+        return max(8.0, (2.0 * obs.radius + 2.0) / 30.0)
+    return 10.0
 
 
 class _WorldView:
@@ -244,6 +247,8 @@ class SimBatch:
         self.agent_index = [(int(w), int(a)) for w in range(self.n_worlds)
                             for a in pw.controlled_ids(w)] if self.n_controlled < 200_000 else None
         self.grid_cell = grid_cell or default_grid_cell(cfg.obs)
+        if cfg.obs.mode == "radial":
+            self.grid_cell = max(self.grid_cell, (2.0 * cfg.obs.radius + 2.0) / 30.0)
         self.layout: DeviceLayout = build_layout(pw, self.grid_cell,
                                                   all_segments=cfg.obs.mode != "radial")
         self._upload()
@@ -282,7 +287,7 @@ class SimBatch:
                      "pt_cell_start", "gpt_x", "gpt_y", "gpt_h", "gpt_kind", "gpt_id",
                      "eseg_cell_start", "eseg_ax", "eseg_ay", "eseg_bx", "eseg_by",
                      "aseg_cell_start", "aseg_ax", "aseg_ay", "aseg_bx", "aseg_by", "aseg_id",
-                     "aseg_edge"):
+                     "aseg_edge", "gpt_xy", "grid_eps"):
             t[name] = _dev(getattr(lay, name), dev)
         t["p_off"] = _dev(pw.p_off, dev)
         t["s_off"] = _dev(pw.s_off, dev)
@@ -292,6 +297,8 @@ class SimBatch:
         tab.n_agents = pw.n_agents
         tab.n_rows = pw.n_controlled
         tab.max_agents = self.max_agents
+        P = np.diff(pw.p_off)
+        tab.max_points = int(P.max()) if len(P) else 0
         for name in N.TABLE_PTRS:
             setattr(tab, name, t[name].data_ptr())
         self._tables = tab
