@@ -136,6 +136,11 @@ def lib():
     return L
 
 
+def lidar_supported() -> bool:
+    """True once the library implements the LiDAR / view-cone kernel."""
+    return hasattr(lib(), "ds_lidar_supported") and bool(lib().ds_lidar_supported())
+
+
 class NativeError(RuntimeError):
     pass
 
