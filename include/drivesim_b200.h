@@ -174,6 +174,8 @@ typedef struct ds_step_args {
 typedef struct ds_handle ds_handle;
 
 int ds_abi_version(void);
+/* 1 when the LiDAR / view-cone observation kernel is built in */
+int ds_lidar_supported(void);
 /* sizeof(ds_config), sizeof(ds_tables), sizeof(ds_state), sizeof(ds_step_args) */
 void ds_struct_sizes(int64_t out[4]);
 const char *ds_last_error(void);

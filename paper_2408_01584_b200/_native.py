@@ -91,7 +91,7 @@ class DsStepArgs(C.Structure):
                 ("reserved0", C.c_int32), ("events", _p * 3)]
 
 
-EXPORTS = ["ds_abi_version", "ds_struct_sizes", "ds_last_error", "ds_create", "ds_destroy", "ds_reset", "ds_step",
+EXPORTS = ["ds_abi_version", "ds_lidar_supported", "ds_struct_sizes", "ds_last_error", "ds_create", "ds_destroy", "ds_reset", "ds_step",
            "ds_observe", "ds_episode_drain", "ds_host_hypot_libm", "ds_host_hypot_cpython",
            "ds_host_hypot_port", "ds_host_wrap_port", "ds_host_road_headings"]
 
@@ -123,7 +123,7 @@ def lib():
     L.ds_host_road_headings.argtypes = [_p, _p, _p, C.c_int64, _p]
     L.ds_host_wrap_port.argtypes = [_p, C.c_int64, _p]
     for n in EXPORTS:
-        if n not in ("ds_abi_version", "ds_last_error", "ds_struct_sizes"):
+        if n not in ("ds_abi_version", "ds_last_error", "ds_struct_sizes", "ds_lidar_supported"):
             getattr(L, n).restype = C.c_int
     if L.ds_abi_version() != ABI_VERSION:
         raise ImportError("libdrivesim_b200.so ABI version mismatch; rebuild")
@@ -138,7 +138,7 @@ def lib():
 
 def lidar_supported() -> bool:
     """True once the library implements the LiDAR / view-cone kernel."""
-    return hasattr(lib(), "ds_lidar_supported") and bool(lib().ds_lidar_supported())
+    return bool(lib().ds_lidar_supported())
 
 
 class NativeError(RuntimeError):

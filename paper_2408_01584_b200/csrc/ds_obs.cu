@@ -632,10 +632,18 @@ cudaError_t configure_kernels(int max_dynamic_smem) {
   e = cudaFuncSetAttribute(obs_radial_kernel<kWarpsGlobal, false>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, max_dynamic_smem);
   if (e != cudaSuccess) return e;
+  e = configure_lidar_kernels(max_dynamic_smem);
+  if (e != cudaSuccess) return e;
   return configure_step_kernels(max_dynamic_smem);
 }
 
 void obs_plan(ds_handle *h, int max_optin) {
+  if (h->cfg.obs_mode != DS_OBS_RADIAL) {
+    h->obs_shared_pts = 0;
+    h->obs_warps = lidar_warps();
+    h->obs_smem = lidar_smem_bytes(h->tab.max_agents, h->obs_width);
+    return;
+  }
   const size_t sh = obs_smem_bytes_shared(h->cfg, h->tab.max_agents, h->tab.max_points);
   if (h->tab.gpt_xy && h->tab.grid_eps && sh <= (size_t)max_optin) {
     h->obs_shared_pts = 1;
@@ -650,7 +658,10 @@ void obs_plan(ds_handle *h, int max_optin) {
 
 cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, float *obs,
                            const float *scale, int32_t *sel_idx, cudaStream_t s) {
-  if (h->cfg.obs_mode != DS_OBS_RADIAL) return cudaErrorNotSupported;
+  if (h->cfg.obs_mode != DS_OBS_RADIAL) {
+    if (sel_idx) return cudaErrorInvalidValue;   // selection indices are radial-only
+    return launch_lidar(h, mask, obs, scale, s);
+  }
   if (h->obs_shared_pts) {
     obs_radial_kernel<kWarpsShared, true><<<h->tab.n_worlds, kWarpsShared * 32, h->obs_smem, s>>>(
         h->tab, h->cfg, h->st, mask, obs, scale, sel_idx, h->obs_width);

@@ -223,8 +223,7 @@ def test_identical_worlds_identical_and_partial_reset(backend):
 @pytest.mark.parametrize("backend", BACKENDS)
 def test_head_rotation_integrates_and_clamps(backend):
     obj = scripted_object(0, hold(0, 0, 0.0, 40), goal=(100, 0))
-    cfg = SimConfig(obs=ObsConfig(mode="view_cone", n_rays=8)) if backend == "oracle" else \
-        SimConfig()
+    cfg = SimConfig(obs=ObsConfig(mode="view_cone", n_rays=8))
     r = Runner([scene([obj])], cfg, backend)
     acts = np.array([[0.0, 0.0, 1.0]])
     r.step(acts)
@@ -328,7 +327,7 @@ def test_translation_and_rotation_invariance(backend):
 
 # -- LiDAR / view cone (test_observation.py:161-281) ------------------------
 
-LIDAR_BACKENDS = ["oracle"]
+LIDAR_BACKENDS = BACKENDS
 
 
 @pytest.mark.parametrize("backend", LIDAR_BACKENDS)
