@@ -253,6 +253,7 @@ class SimBatch:
                                                   all_segments=cfg.obs.mode != "radial")
         self._upload()
         self._episode_infos: list = []
+        self._by_serial: dict = {}
         self._serial = 0
         self._steps_since_drain = 0
         self._handle = C.c_void_p()
@@ -436,8 +437,19 @@ class SimBatch:
             recs = recs[np.lexsort((recs[:, 1], recs[:, 0]))]
             names = self.packed.names
             for serial, w, nc, ng, nv, no in recs.tolist():
-                self._episode_infos.append(EpisodeInfo(names[w], w, nc, ng, nv, no))
+                e = EpisodeInfo(names[w], w, nc, ng, nv, no)
+                self._episode_infos.append(e)
+                self._by_serial.setdefault(serial, []).append(e)
+        # keep per-step lists only for the recent window (lazy env readers)
+        old = [k for k in self._by_serial if k < self._serial - 4 * self.RING_STEPS]
+        for k in old:
+            del self._by_serial[k]
         N.check(rc, "ds_episode_drain")
+
+    def episodes_of_step(self, serial: int) -> list:
+        """Episode records finished during step ``serial`` (synchronises)."""
+        self._drain()
+        return self._by_serial.pop(serial, [])
 
     @property
     def episode_infos(self) -> list:

@@ -111,3 +111,42 @@ def preprocess(s: Scenario, decimation_threshold: float = 0.0,
     ctrl = mark_controllable(s, controllable_threshold)
     return PreparedScenario(base=s, decimated_roads=roads, controllable=ctrl,
                             stats=PrepStats(len(s.objects), sum(ctrl), n_pts, n_pts))
+
+
+def load_prepared(json_text: str) -> PreparedScenario:
+    """Minimal reader of the reference's prepared-scenario JSON
+    (scenario.py:418-454: scenario fields plus a "prepared" section); plain
+    scenario files are preprocessed with decimation 0.  No schema validation
+    (ingestion is out of scope)."""
+    import json
+    doc = json.loads(json_text)
+    objs = []
+    for raw in doc.get("objects", []):
+        states = [LoggedStep(position=Vec2(*map(float, st["p"])), heading=float(st["heading"]),
+                             velocity=Vec2(*map(float, st["v"])), valid=bool(st.get("valid", True)))
+                  for st in raw["states"]]
+        if "goal" in raw:
+            goal = Vec2(*map(float, raw["goal"]))
+        else:
+            goal = next(s.position for s in reversed(states) if s.valid)
+        objs.append(ObjectLog(id=int(raw["id"]), kind=raw["type"], length=float(raw["length_m"]),
+                              width=float(raw["width_m"]), goal=goal, states=states,
+                              force_replay=bool(raw.get("force_replay", False))))
+    roads = [RoadElement(id=int(r["id"]), kind=r["type"],
+                         geometry=[Vec2(float(x), float(y)) for x, y in r["geometry"]])
+             for r in doc.get("roads", [])]
+    base = Scenario(name=doc["name"], timestep=float(doc.get("timestep_s", DEFAULT_TIMESTEP)),
+                    num_steps=int(doc.get("num_steps", DEFAULT_NUM_STEPS)), objects=objs,
+                    roads=roads)
+    prep = doc.get("prepared")
+    if not isinstance(prep, dict):
+        return preprocess(base)
+    dec = [RoadElement(id=int(r["id"]), kind=r["type"],
+                       geometry=[Vec2(float(x), float(y)) for x, y in r["geometry"]])
+           for r in prep["roads"]]
+    st = prep["stats"]
+    return PreparedScenario(base=base, decimated_roads=dec,
+                            controllable=[bool(b) for b in prep["controllable"]],
+                            stats=PrepStats(int(st["n_objects"]), int(st["n_controllable"]),
+                                            int(st["n_road_points_before"]),
+                                            int(st["n_road_points_after"])))
