@@ -146,6 +146,11 @@ typedef struct ds_state {
   uint32_t *ring_head;
   int32_t ring_cap;
   int32_t reserved0;
+  /* [n_agents][4] search hint of the radial observation: a bound on the
+   * k-th road-point distance and the (grid-relative) position it was taken
+   * at; results never depend on it (it only narrows a provably sufficient
+   * search disc).  NULL disables it. */
+  float *obs_hint;
 } ds_state;
 
 /* Per-call step arguments. */

@@ -79,7 +79,7 @@ STATE_PTRS = ["x", "y", "heading", "speed", "head_angle", "flags", "t", "episode
 
 class DsState(C.Structure):
     _fields_ = [(n, _p) for n in STATE_PTRS] + [("ring_cap", C.c_int32),
-                                                ("reserved0", C.c_int32)]
+                                                ("reserved0", C.c_int32), ("obs_hint", _p)]
 
 
 class DsStepArgs(C.Structure):

@@ -32,7 +32,7 @@ namespace ds {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNB = 256;       // histogram buckets
 constexpr int kCand = 640;     // buffered pass-1 candidates (global-points variant)
-constexpr int kWarpsShared = 24;
+constexpr int kWarpsShared = 20;
 constexpr int kWarpsGlobal = 12;
 
 __host__ __device__ inline int kmax_of(const ds_config &c) {
@@ -50,7 +50,7 @@ __host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~size_t(15)
 // block (11 floats per slot) aliases [hc ..), which is dead once the road
 // selection has produced sel_pl.
 struct WarpLayout {
-  size_t row, hc, ca, cp, ge, gid, gpl, gb, sel_pl, sel_id, total;
+  size_t row, hc, ca, cp, ga, ge, gid, gpl, gb, gf, sel_pl, sel_id, total;
 };
 
 __host__ __device__ inline WarpLayout warp_layout(const ds_config &c, bool buffered) {
@@ -62,10 +62,12 @@ __host__ __device__ inline WarpLayout warp_layout(const ds_config &c, bool buffe
   L.hc = o; o = al16(o + kNB * sizeof(uint32_t));
   L.ca = o; if (buffered) o = al16(o + kCand * sizeof(float));
   L.cp = o; if (buffered) o = al16(o + kCand * sizeof(uint16_t));
+  L.ga = o; o = al16(o + gc * sizeof(float));
   L.ge = o; o = al16(o + gc * sizeof(double));
   L.gid = o; o = al16(o + gc * sizeof(int));
   L.gpl = o; o = al16(o + gc * sizeof(int));
   L.gb = o; o = al16(o + gc);
+  L.gf = o; o = al16(o + gc);
   const size_t road_end = al16(L.hc + (size_t)c.max_road_points_obs * 11 * sizeof(float));
   if (o < road_end) o = road_end;
   L.sel_pl = o; o = al16(o + km * sizeof(int));
@@ -91,9 +93,10 @@ struct Sel {
   uint32_t *hc;
   float *ca;
   uint16_t *cp;
+  float *ga;
   double *ge;
   int *gid, *gpl;
-  uint8_t *gb;
+  uint8_t *gb, *gf;
   int *sel_pl, *sel_id;
   int gcap;
 };
@@ -150,6 +153,43 @@ struct RowGeo {
   }
 };
 
+// Non-empty cell rows compacted to lanes 0..n-1 with inclusive prefix ends,
+// so candidates are visited in full 32-wide batches across row boundaries.
+// Lane o of the batch starting at f0 maps to row #(ends <= f0) plus the
+// number of row ends inside (f0, f0 + o]: one OR-reduction of end offsets
+// and a popcount (ends are distinct because empty rows were dropped).
+struct FlatRows {
+  int sb, cnt, pe, nr, total;
+  __device__ __forceinline__ void build(int sb_in, int cnt_in, int lane) {
+    const unsigned bal = __ballot_sync(kFull, cnt_in > 0);
+    nr = __popc(bal);
+    int src = (int)__fns(bal, 0, lane + 1);
+    src = (src >= 0 && src < 32) ? src : 0;
+    sb = __shfl_sync(kFull, sb_in, src);
+    cnt = __shfl_sync(kFull, cnt_in, src);
+    if (lane >= nr) cnt = 0;
+    pe = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int up = __shfl_up_sync(kFull, pe, off);
+      if (lane >= off) pe += up;
+    }
+    total = __shfl_sync(kFull, pe, 31);
+  }
+  // point index of flattened candidate f0 + lane (valid when f0 + lane < total)
+  __device__ __forceinline__ int map(int f0, int lane) const {
+    const bool live = lane < nr;
+    const int r0 = __popc(__ballot_sync(kFull, live && pe <= f0));
+    const int off = pe - f0;
+    const unsigned E = __reduce_or_sync(kFull, (live && off > 0 && off < 32) ? (1u << off) : 0u);
+    const int r = (r0 + __popc(E & ((2u << lane) - 1u))) & 31;
+    const int rs = __shfl_sync(kFull, sb, r);
+    const int rpe = __shfl_sync(kFull, pe, r);
+    const int rc = __shfl_sync(kFull, cnt, r);
+    return rs + (f0 + lane - (rpe - rc));
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Candidate sources.  visit(r2hi, lane, fn) calls fn(ok, key, payload)
 // warp-collectively, one candidate per lane; exact(payload, id) returns the
@@ -193,36 +233,32 @@ struct RoadSrcShared {
   const float2 *pts;                 // shared, world-relative index
   const double *__restrict__ gx, *__restrict__ gy;
   const int *__restrict__ gid;
-  int sb, cnt, nrows, p0;            // sb relative to p0
+  int p0;
   float prx, pry;
   double px, py;
   const RowGeo *geo;
-  // shrink the scanned rows to the disc of radius rho (pass 2)
-  __device__ __forceinline__ void restrict_to(double rho, int lane) {
+  FlatRows rows;
+  __device__ __forceinline__ void cover(double rho, int lane) {
     int b, c;
     geo->range(rho, lane, b, c);
-    sb = b - p0;
-    cnt = c;
+    rows.build(b - p0, c, lane);
   }
+  __device__ __forceinline__ void restrict_to(double rho, int lane) { cover(rho, lane); }
   __device__ __forceinline__ int pbase() const { return 0; }
   __device__ __forceinline__ bool small_payload() const { return true; }
   template <class F>
   __device__ __forceinline__ void visit(float r2hi, int lane, F &&fn) const {
-    for (int r = 0; r < nrows; ++r) {
-      const int rb = __shfl_sync(kFull, sb, r);
-      const int rc = __shfl_sync(kFull, cnt, r);
-      for (int j0 = 0; j0 < rc; j0 += 32) {
-        const int j = j0 + lane;
-        bool ok = j < rc;
-        float a = 0.0f;
-        if (ok) {
-          const float2 p = pts[rb + j];
-          const float dx = p.x - prx, dy = p.y - pry;
-          a = fmaf(dx, dx, dy * dy);
-          ok = a <= r2hi;
-        }
-        fn(ok, a, rb + j);
+    for (int f0 = 0; f0 < rows.total; f0 += 32) {
+      const int s = rows.map(f0, lane);
+      bool ok = f0 + lane < rows.total;
+      float a = 0.0f;
+      if (ok) {
+        const float2 p = pts[s];
+        const float dx = p.x - prx, dy = p.y - pry;
+        a = fmaf(dx, dx, dy * dy);
+        ok = a <= r2hi;
       }
+      fn(ok, a, s);
     }
   }
   __device__ __forceinline__ double exact(int pl, int &id) const {
@@ -235,28 +271,30 @@ struct RoadSrcShared {
 struct RoadSrcGlobal {
   const double *__restrict__ gx, *__restrict__ gy;
   const int *__restrict__ gid;
-  int sb, cnt, nrows, p0, np;        // sb absolute
+  int p0, np;
   double px, py;
   const RowGeo *geo;
-  __device__ __forceinline__ void restrict_to(double rho, int lane) { geo->range(rho, lane, sb, cnt); }
+  FlatRows rows;
+  __device__ __forceinline__ void cover(double rho, int lane) {
+    int b, c;
+    geo->range(rho, lane, b, c);
+    rows.build(b, c, lane);
+  }
+  __device__ __forceinline__ void restrict_to(double rho, int lane) { cover(rho, lane); }
   __device__ __forceinline__ int pbase() const { return p0; }
   __device__ __forceinline__ bool small_payload() const { return np <= 0xffff; }
   template <class F>
   __device__ __forceinline__ void visit(float r2hi, int lane, F &&fn) const {
-    for (int r = 0; r < nrows; ++r) {
-      const int rb = __shfl_sync(kFull, sb, r);
-      const int rc = __shfl_sync(kFull, cnt, r);
-      for (int j0 = 0; j0 < rc; j0 += 32) {
-        const int j = j0 + lane;
-        bool ok = j < rc;
-        float a = 0.0f;
-        if (ok) {
-          const double dx = gx[rb + j] - px, dy = gy[rb + j] - py;
-          a = (float)fma(dx, dx, dy * dy);
-          ok = a <= r2hi;
-        }
-        fn(ok, a, rb + j);
+    for (int f0 = 0; f0 < rows.total; f0 += 32) {
+      const int s = rows.map(f0, lane);
+      bool ok = f0 + lane < rows.total;
+      float a = 0.0f;
+      if (ok) {
+        const double dx = gx[s] - px, dy = gy[s] - py;
+        a = (float)fma(dx, dx, dy * dy);
+        ok = a <= r2hi;
       }
+      fn(ok, a, s);
     }
   }
   __device__ __forceinline__ double exact(int pl, int &id) const {
@@ -320,61 +358,102 @@ __device__ int select_serial(const Src &src, int k, double radius, float r2hi, c
 }
 
 // Exact ascending top-min(n_valid, k) by (distance, id) given candidate keys
-// with |a - d^2| <= D.  Payloads land in S.sel_pl[0..m), ids in S.sel_id.
-// Warp-collective.  Buffered: pass 1 keeps (key, payload) in shared memory.
+// with |a - d^2| <= D.  Payloads land in S.sel_pl[0..m).  Warp-collective.
+//  * rho: the radius the source currently covers (< radius when the caller
+//    narrowed it with a search hint, see hint_radius).  A narrowed pass 1 is
+//    used only if every bucket the selection touches provably lies inside
+//    the disc ((bmax + 1) w + D <= rho^2), else it reruns on the full radius.
+//    On return, bound_out holds a bound on the k-th distance (0 when fewer
+//    than k candidates exist).
+//  * ranking uses the float keys: two keys more than 2D apart are ordered
+//    exactly as the distances, so the exact FP64 hypot is evaluated only for
+//    near ties (|a_p - a_q| <= 2D) and possible out-of-radius keys.
+// Buffered: pass 1 keeps (key, payload) in shared memory (global-points path).
+__device__ __forceinline__ double sel_r2hi(double radius, double D) {
+  return (double)(float)((radius * radius + D) * (1.0 + 1e-7) + 1e-30);
+}
+
+// Radius that provably contains the k nearest candidates given a hint that
+// bounds the k-th distance (triangle inequality), widened so that the
+// selection's bucket window (b* + 2) stays inside it.
+__device__ __forceinline__ double hint_radius(double hint, double radius, double D) {
+  if (!(hint > 0.0)) return radius;
+  const double w = sel_r2hi(radius, D) / kNB;
+  return fmin(sqrt(hint * hint + 3.1 * w + D) + 1e-3, radius);
+}
+
 template <bool Buffered, class Src>
-__device__ int select_topk(Src src, int k, double radius, double D, const Sel &S, int lane) {
+__device__ int select_topk(Src src, int k, double radius, double D, const Sel &S, int lane,
+                           double rho, float &bound_out) {
   if (k <= 0) return 0;
   const double r2 = radius * radius;
   const float r2hi = (float)((r2 + D) * (1.0 + 1e-7) + 1e-30);
   const float inv_w = r2hi > 0.0f ? (float)kNB / r2hi : 0.0f;
+  const double w = (double)r2hi / kNB;
   // edge band in bucket units: twice the key error plus float slack
   const float beta = (float)(2.0 * D * (double)inv_w) + 4e-5f;
   if (!(beta < 0.125f)) return select_serial(src, k, radius, r2hi, S, lane);
-  for (int b = lane; b < kNB; b += 32) S.hc[b] = 0u;
-  __syncwarp();
+  // near-tie band in float, padded by the float rounding of a - 2D
+  const float two_d = (float)(2.0 * D + 2.5e-7 * (double)r2hi);
+  bool restricted = rho < radius;
   const int pb = src.pbase();
-  int nbuf = 0;
-  src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
-    if (ok) atomicAdd(&S.hc[bucket_of(a, inv_w)], 1u);
-    if (Buffered) {
-      const unsigned bal = __ballot_sync(kFull, ok);
-      const int pos = nbuf + __popc(bal & ((1u << lane) - 1u));
-      if (ok && pos < kCand) {
-        S.ca[pos] = a;
-        S.cp[pos] = (uint16_t)(pl - pb);
-      }
-      nbuf += __popc(bal);
-    }
-  });
-  __syncwarp();
   constexpr int kPer = kNB / 32;
+  uint32_t total, n_g, incl, local;
   uint32_t cnt[kPer];
-  uint32_t local = 0;
+  int bstar, bmax, nbuf;
+  while (true) {
+    for (int b = lane; b < kNB; b += 32) S.hc[b] = 0u;
+    __syncwarp();
+    nbuf = 0;
+    src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
+      if (ok) atomicAdd(&S.hc[bucket_of(a, inv_w)], 1u);
+      if (Buffered) {
+        const unsigned bal = __ballot_sync(kFull, ok);
+        const int pos = nbuf + __popc(bal & ((1u << lane) - 1u));
+        if (ok && pos < kCand) {
+          S.ca[pos] = a;
+          S.cp[pos] = (uint16_t)(pl - pb);
+        }
+        nbuf += __popc(bal);
+      }
+    });
+    __syncwarp();
+    local = 0;
 #pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    cnt[q] = S.hc[lane * kPer + q];
-    local += cnt[q];
-  }
-  uint32_t incl = local;
+    for (int q = 0; q < kPer; ++q) {
+      cnt[q] = S.hc[lane * kPer + q];
+      local += cnt[q];
+    }
+    incl = local;
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t up = __shfl_up_sync(kFull, incl, off);
-    if (lane >= off) incl += up;
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t up = __shfl_up_sync(kFull, incl, off);
+      if (lane >= off) incl += up;
+    }
+    total = __shfl_sync(kFull, incl, 31);
+    uint32_t run = incl - local;
+    bstar = kNB - 1;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      if (run < (uint32_t)k && run + cnt[q] >= (uint32_t)k) bstar = lane * kPer + q;
+      run += cnt[q];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) bstar = min(bstar, __shfl_xor_sync(kFull, bstar, off));
+    bmax = min(bstar + 2, kNB - 1);
+    // restricted scan valid only if all buckets <= bmax lie inside the disc
+    if (restricted && !((((double)bmax + 1.01) * w + D) <= rho * rho)) {
+      src.restrict_to(radius + 1e-6, lane);
+      restricted = false;
+      continue;
+    }
+    break;
   }
-  const uint32_t total = __shfl_sync(kFull, incl, 31);
+  bound_out = total >= (uint32_t)k ? (float)(sqrt(((double)bstar + 1.0) * w + D) * (1.0 + 1e-6))
+                                    : 0.0f;
   if (total == 0) return 0;
-  uint32_t run = incl - local;
-  int bstar = kNB - 1;
-#pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    if (run < (uint32_t)k && run + cnt[q] >= (uint32_t)k) bstar = lane * kPer + q;
-    run += cnt[q];
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) bstar = min(bstar, __shfl_xor_sync(kFull, bstar, off));
-  const int bmax = min(bstar + 2, kNB - 1);
-  uint32_t run2 = incl - local, n_g = 0;
+  uint32_t run2 = incl - local;
+  n_g = 0;
 #pragma unroll
   for (int q = 0; q < kPer; ++q) {
     const int b = lane * kPer + q;
@@ -385,68 +464,107 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) n_g = max(n_g, __shfl_xor_sync(kFull, n_g, off));
   __syncwarp();
-  if (n_g > (uint32_t)S.gcap || total > 0xffffu)
+  if (n_g > (uint32_t)S.gcap || total > 0xffffu) {
+    src.restrict_to(radius + 1e-6, lane);
     return select_serial(src, k, radius, r2hi, S, lane);
+  }
   // pass 2: counting-sort scatter of buckets <= bmax into G
   auto scatter = [&](float a, int pl) {
     const int b = bucket_of(a, inv_w);
     if (b <= bmax) {
       const uint32_t pos = atomicAdd(&S.hc[b], 1u << 16) >> 16;
+      S.ga[pos] = a;
       S.gpl[pos] = pl;
       S.gb[pos] = (uint8_t)b;
-      S.ge[pos] = (double)a;   // key parked for the edge test
     }
   };
   if (Buffered && nbuf <= kCand && src.small_payload()) {
     for (int p = lane; p < nbuf; p += 32) scatter(S.ca[p], pb + (int)S.cp[p]);
   } else {
     // only keys in buckets <= bmax matter: a < (bmax + 1) w, so d^2 < that + D
-    if (bmax < kNB - 1) src.restrict_to(sqrt(((double)bmax + 1.001) / (double)inv_w + D) + 1e-6, lane);
+    if (bmax < kNB - 1) src.restrict_to(sqrt(((double)bmax + 1.01) * w + D) + 1e-6, lane);
     src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
       if (ok) scatter(a, pl);
     });
   }
   __syncwarp();
-  // exact keys for G; out-of-radius -> +inf (never counted, never selected);
-  // the edge flag rides in the payload's complement until ranking
-  int n_valid = 0;
+  // phase A: rank by float key; flag near ties and possibly-out-of-radius keys
+  int flagged = 0;
   for (int p = lane; p < (int)n_g; p += 32) {
-    const float t = (float)S.ge[p] * inv_w;
+    const float ap = S.ga[p];
+    const int b = S.gb[p];
+    const float t = ap * inv_w;
     const float fr = t - floorf(t);
     const bool edge = fr < beta || fr > 1.0f - beta;
-    int id;
-    const int pl = S.gpl[p];
-    const double e = src.exact(pl, id);
-    const bool v = e <= radius;
-    S.ge[p] = v ? e : INFINITY;
-    S.gid[p] = id;
-    if (edge) S.gpl[p] = ~pl;
-    n_valid += v;
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) n_valid += __shfl_xor_sync(kFull, n_valid, off);
-  __syncwarp();
-  // exact rank: own bucket, or across the adjacent buckets for edge elements
-  for (int p = lane; p < (int)n_g; p += 32) {
-    const double ep = S.ge[p];
-    if (ep == INFINITY) continue;
-    const int plp = S.gpl[p];
-    const bool edge = plp < 0;
-    const int ip = S.gid[p];
-    const int b = S.gb[p];
     const int lo = edge ? (b > 0 ? b - 1 : 0) : b;
     const int hi = edge ? (b < bmax ? b + 1 : bmax) : b;
     const uint32_t hlo = S.hc[lo], hhi = S.hc[hi];
     const int start = (int)(hlo >> 16) - (int)(hlo & 0xffffu);
     const int end = (int)(hhi >> 16);
+    const float dlo = ap - two_d, dhi = ap + two_d;
     int rank = start;
-    for (int q = start; q < end; ++q) rank += key_less(S.ge[q], S.gid[q], ep, ip) ? 1 : 0;
-    if (rank < k) {
-      S.sel_pl[rank] = edge ? ~plp : plp;
-      S.sel_id[rank] = ip;
+    bool amb = false;
+    for (int q = start; q < end; ++q) {
+      if (q == p) continue;
+      const float aq = S.ga[q];
+      rank += aq < dlo ? 1 : 0;
+      amb |= aq >= dlo && aq <= dhi;
     }
+    const uint8_t f = (amb ? 1 : 0) | ((double)ap > r2 - D ? 2 : 0) | (edge ? 8 : 0);
+    S.gf[p] = f;
+    if (!(f & 3) && rank < k) S.sel_pl[rank] = S.gpl[p];
+    flagged += (f & 3) != 0;
+  }
+  int n_invalid = 0;
+  if (__any_sync(kFull, flagged)) {
+    __syncwarp();
+    // phase B: exact (distance, id) of the flagged elements
+    for (int p = lane; p < (int)n_g; p += 32) {
+      const uint8_t f = S.gf[p];
+      if (!(f & 3)) continue;
+      int id;
+      const double e = src.exact(S.gpl[p], id);
+      S.ge[p] = e;
+      S.gid[p] = id;
+      if (e > radius) {
+        S.gf[p] = f | 4;
+        ++n_invalid;
+      }
+    }
+    __syncwarp();
+    // phase C: rank the valid flagged elements (near ties compared exactly;
+    // ambiguity is symmetric, so both ends of a near tie carry exact keys)
+    for (int p = lane; p < (int)n_g; p += 32) {
+      const uint8_t f = S.gf[p];
+      if (!(f & 3) || (f & 4)) continue;
+      const float ap = S.ga[p];
+      const int b = S.gb[p];
+      const bool edge = f & 8;
+      const int lo = edge ? (b > 0 ? b - 1 : 0) : b;
+      const int hi = edge ? (b < bmax ? b + 1 : bmax) : b;
+      const uint32_t hlo = S.hc[lo], hhi = S.hc[hi];
+      const int start = (int)(hlo >> 16) - (int)(hlo & 0xffffu);
+      const int end = (int)(hhi >> 16);
+      const float dlo = ap - two_d, dhi = ap + two_d;
+      const double ep = S.ge[p];
+      const int ip = S.gid[p];
+      int rank = start;
+      for (int q = start; q < end; ++q) {
+        if (q == p) continue;
+        const float aq = S.ga[q];
+        if (aq < dlo) {
+          ++rank;
+        } else if (aq <= dhi) {
+          if (!(S.gf[q] & 4) && key_less(S.ge[q], S.gid[q], ep, ip)) ++rank;
+        }
+      }
+      if (rank < k) S.sel_pl[rank] = S.gpl[p];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) n_invalid += __shfl_xor_sync(kFull, n_invalid, off);
   }
   __syncwarp();
+  const int n_valid = (int)n_g - n_invalid;
   return n_valid < k ? n_valid : k;
 }
 
@@ -480,10 +598,12 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
   S.hc = reinterpret_cast<uint32_t *>(wb + WL.hc);
   S.ca = reinterpret_cast<float *>(wb + WL.ca);
   S.cp = reinterpret_cast<uint16_t *>(wb + WL.cp);
+  S.ga = reinterpret_cast<float *>(wb + WL.ga);
   S.ge = reinterpret_cast<double *>(wb + WL.ge);
   S.gid = reinterpret_cast<int *>(wb + WL.gid);
   S.gpl = reinterpret_cast<int *>(wb + WL.gpl);
   S.gb = wb + WL.gb;
+  S.gf = wb + WL.gf;
   S.sel_pl = reinterpret_cast<int *>(wb + WL.sel_pl);
   S.sel_id = reinterpret_cast<int *>(wb + WL.sel_id);
   S.gcap = gcap_of(C);
@@ -549,7 +669,8 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
 
     // ---- partners
     PartnerSrc psrc{ax, ay, avis, A, i, px, py};
-    const int ma = select_topk<false>(psrc, cap_a, radius, D_fp64, S, lane);
+    float no_bound = 0.0f;
+    const int ma = select_topk<false>(psrc, cap_a, radius, D_fp64, S, lane, radius, no_bound);
     float *ps = row + 7;
     for (int m = lane; m < ma; m += 32) {
       const int j = S.sel_pl[m];
@@ -571,11 +692,18 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
 
     // ---- road points: lane l owns cell row iy0 + l of the disc
     int mr = 0;
+    // search hint: (bound on the k-th road distance, position it was taken at)
+    float4 hint = St.obs_hint ? reinterpret_cast<const float4 *>(St.obs_hint)[g]
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+    float bound = 0.0f;
+    double rho_hint = 0.0;
+    if (hint.x > 0.0f) {
+      const double mx = (double)hint.y - (px - gx0), my = (double)hint.z - (py - gy0);
+      rho_hint = (double)hint.x + sqrt(mx * mx + my * my) + 1e-3;
+    }
     if (cap_r > 0) {
       RowGeo geo{T.pt_cell_start + cbase, px, py, gx0, gy0, cs, inv_cs, nx, ny, 0, 0};
       geo.init(reach);
-      int sb, cnt;
-      geo.range(reach, lane, sb, cnt);
       if (SharedPts) {
         const double rx = px - gx0, ry = py - gy0;
         const float prx = (float)rx, pry = (float)ry;
@@ -583,14 +711,20 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
         const double E = eps_p + fmax(fabs((double)prx - rx), fabs((double)pry - ry)) +
                          (radius + 1.0) * 1.2e-7;
         const double D = 4.0 * (radius + 1.0) * E + 2.0 * E * E + D_fp64;
-        RoadSrcShared rsrc{pts, T.gpt_x, T.gpt_y, T.gpt_id, sb - (int)p0, cnt, geo.nrows, (int)p0,
-                           prx, pry, px, py, &geo};
-        mr = select_topk<false>(rsrc, cap_r, radius, D, S, lane);
+        const double rho = hint_radius(rho_hint, radius, D);
+        RoadSrcShared rsrc{pts, T.gpt_x, T.gpt_y, T.gpt_id, (int)p0, prx, pry, px, py, &geo};
+        rsrc.cover(rho < radius ? rho : reach, lane);
+        mr = select_topk<false>(rsrc, cap_r, radius, D, S, lane, rho, bound);
       } else {
-        RoadSrcGlobal rsrc{T.gpt_x, T.gpt_y, T.gpt_id, sb, cnt, geo.nrows, (int)p0, np, px, py, &geo};
-        mr = select_topk<true>(rsrc, cap_r, radius, D_fp64, S, lane);
+        const double rho = hint_radius(rho_hint, radius, D_fp64);
+        RoadSrcGlobal rsrc{T.gpt_x, T.gpt_y, T.gpt_id, (int)p0, np, px, py, &geo};
+        rsrc.cover(rho < radius ? rho : reach, lane);
+        mr = select_topk<true>(rsrc, cap_r, radius, D_fp64, S, lane, rho, bound);
       }
     }
+    if (St.obs_hint && lane == 0)
+      reinterpret_cast<float4 *>(St.obs_hint)[g] =
+          make_float4(bound, (float)(px - gx0), (float)(py - gy0), 0.0f);
     // road block staged as the final 11-float slots (aliases the dead scratch)
     float *rstage = row + road_off;
     const int sel_off = SharedPts ? (int)p0 : 0;
@@ -606,7 +740,7 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
 #pragma unroll
         for (int q = 0; q < 7; ++q) slot[3 + q] = q == kind ? 1.0f : 0.0f;
         slot[10] = 1.0f;
-        if (sel_idx) sel_idx[orow * sel_w + cap_a + m] = S.sel_id[m];
+        if (sel_idx) sel_idx[orow * sel_w + cap_a + m] = T.gpt_id[s];
       } else {
 #pragma unroll
         for (int q = 0; q < 11; ++q) slot[q] = 0.0f;

@@ -325,6 +325,8 @@ class SimBatch:
                           ("ring", self._ring), ("ring_head", self._ring_head)):
             setattr(st, name, ten.data_ptr())
         st.ring_cap = self._ring_cap
+        self._hint = torch.zeros((max(n, 1), 4), dtype=torch.float32, device=dev)
+        st.obs_hint = self._hint.data_ptr()
         self._state = st
 
         # Outputs (reused every call, like the reference's buffers).
