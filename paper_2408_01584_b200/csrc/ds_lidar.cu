@@ -33,21 +33,40 @@ __host__ __device__ inline size_t lidar_agents_bytes(int amax) {
   return al16l((size_t)amax * (7 * sizeof(double) + 1));
 }
 
+__host__ __device__ inline size_t lidar_warp_bytes(int obs_width, int n_rays) {
+  return al16l((size_t)n_rays * 3 * sizeof(double) + (size_t)obs_width * sizeof(float));
+}
+
 __device__ __forceinline__ int clampl(double f, int lo, int hi) {
   if (f < (double)lo) return lo;
   if (f > (double)hi) return hi;
   return (int)f;
 }
 
-// raycast_segments_arr (geo:380-396) for one ray and one segment; inf = miss.
+// raycast_segments_arr (geo:380-396) for one ray and one segment, returning
+// the reference's t (inf = miss) -- but only when it can be <= `beat`: the
+// signs and magnitudes of the numerators decide most misses exactly without
+// dividing (division preserves signs; |un| > |den| (1 + 2^-50) implies u > 1;
+// |tn| > beat |den| (1 + 2^-50) implies t > beat); the reference's divisions
+// run only for candidate hits.
 __device__ __forceinline__ double ray_segment(double ox, double oy, double dx, double dy,
-                                              double ax, double ay, double bx, double by) {
+                                              double ax, double ay, double bx, double by,
+                                              double beat) {
   const double ex = bx - ax, ey = by - ay;
   const double wx = ax - ox, wy = ay - oy;
   const double denom = dx * ey - dy * ex;
   if (denom == 0.0) return INFINITY;
-  const double t = (wx * ey - wy * ex) / denom;
-  const double u = (wx * dy - wy * dx) / denom;
+  const double tn = wx * ey - wy * ex;
+  const double un = wx * dy - wy * dx;
+  const double ad = fabs(denom);
+  const double ts = denom < 0.0 ? -tn : tn, us = denom < 0.0 ? -un : un;
+  // negative quotients (a tiny one could underflow to -0, so keep a guard)
+  if (ts < 0.0 && -ts > ad * 1e-280) return INFINITY;
+  if (us < 0.0 && -us > ad * 1e-280) return INFINITY;
+  if (us > ad * (1.0 + 1e-15)) return INFINITY;
+  if (ts > beat * ad * (1.0 + 1e-15)) return INFINITY;
+  const double t = tn / denom;
+  const double u = un / denom;
   if (t >= 0.0 && u >= 0.0 && u <= 1.0) return t;
   return INFINITY;
 }
@@ -103,6 +122,7 @@ __device__ double walk_segments(const SegGrid &G, double ox, double oy, double d
   const int iya = clampl(floor((oy - G.gy0) * G.inv_cs), -1, G.ny);
   const int iyb = clampl(floor((y_end - G.gy0) * G.inv_cs), -1, G.ny);
   const int step = iyb >= iya ? 1 : -1;
+  const double inv_dy = dy != 0.0 ? 1.0 / dy : 0.0;
   for (int iy = iya;; iy += step) {
     if (iy >= 0 && iy < G.ny) {
       const double ylo = G.gy0 + iy * G.cs - slack, yhi = G.gy0 + (iy + 1) * G.cs + slack;
@@ -116,9 +136,9 @@ __device__ double walk_segments(const SegGrid &G, double ox, double oy, double d
           t1 = limit;
         }
       } else {
-        const double ta = (ylo - oy) / dy, tb = (yhi - oy) / dy;
-        t0 = fmax(0.0, fmin(ta, tb));
-        t1 = fmin(limit, fmax(ta, tb));
+        const double ta = (ylo - oy) * inv_dy, tb = (yhi - oy) * inv_dy;
+        t0 = fmax(0.0, fmin(ta, tb) - 1e-9);
+        t1 = fmin(limit, fmax(ta, tb) + 1e-9);
       }
       if (t0 > best) break;   // bands further out only hold larger distances
       if (t0 <= t1) {
@@ -130,7 +150,9 @@ __device__ double walk_segments(const SegGrid &G, double ox, double oy, double d
           const int *c = G.cell_start + (int64_t)iy * G.nx;
           const int b = c[ix0], e = c[ix1 + 1];
           for (int k = b; k < e; ++k) {
-            const double t = ray_segment(ox, oy, dx, dy, G.ax[k], G.ay[k], G.bx[k], G.by[k]);
+            const double beat = best < limit ? best : limit;
+            const double t =
+                ray_segment(ox, oy, dx, dy, G.ax[k], G.ay[k], G.bx[k], G.by[k], beat);
             if (t < best || (t == best && G.sid[k] < best_id)) {
               if (t != INFINITY) {
                 best = t;
@@ -166,8 +188,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
          *shw = sx + 5 * amax, *scr = sx + 6 * amax;
   uint8_t *svis = reinterpret_cast<uint8_t *>(sx + 7 * amax);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float *row = reinterpret_cast<float *>(smem_raw + lidar_agents_bytes(amax)) +
-               (size_t)warp * ((obs_width + 3) & ~3);
+  const size_t per_warp = lidar_warp_bytes(obs_width, C.n_rays);
+  unsigned char *wb = smem_raw + lidar_agents_bytes(amax) + (size_t)warp * per_warp;
+  double *rdx = reinterpret_cast<double *>(wb);
+  double *rdy = rdx + C.n_rays;
+  unsigned long long *rbest = reinterpret_cast<unsigned long long *>(rdy + C.n_rays);
+  float *row = reinterpret_cast<float *>(rbest + C.n_rays);
 
   const int64_t a0 = T.a_off[w];
   const int A = (int)(T.a_off[w + 1] - a0);
@@ -226,35 +252,73 @@ __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
     }
     double center = h;
     if (C.obs_mode == DS_OBS_VIEW_CONE) center += St.head_angle[g];
-    // candidate boxes (visible, not ego, within max_range + circumradius),
-    // one ballot word per 32 agents
+    // ray directions (_ray_angles, obs:213-220) and per-ray box minima
     for (int k = lane; k < R; k += 32) {
       double ang;
       if (full_circle) ang = center + (2.0 * kPi * (double)k) / (double)R;
       else if (R == 1) ang = center;
       else ang = (center - 0.5 * C.fov) + (C.fov * (double)k) / (double)(R - 1);
-      const double dx = cos(ang), dy = sin(ang);
-      double best = INFINITY;
-      int type = 3;
-      // boxes
-      double bmin = INFINITY;
-      for (int j = 0; j < A; ++j) {
-        if (j == i || !svis[j]) continue;
-        const double cx = sx[j] - ox, cy = sy[j] - oy;
-        const double cr = scr[j];
-        // cheap superset reject: ray line farther than the circumradius from
-        // the centre, or the whole disc behind the origin
-        const double proj = cx * dx + cy * dy;
-        const double perp = fabs(cx * dy - cy * dx);
-        if (perp > cr + 1e-3 || proj < -cr - 1e-3) continue;
-        if (!(hypot(cx, cy) <= max_range + cr)) continue;
-        const double d = ray_box(ox, oy, dx, dy, sx[j], sy[j], sc[j], ss[j], shl[j], shw[j]);
-        if (d < bmin) bmin = d;
+      rdx[k] = cos(ang);
+      rdy[k] = sin(ang);
+      rbest[k] = 0x7ff0000000000000ull;   // +inf
+    }
+    __syncwarp();
+    // boxes, box-major: the reference's candidates (visible, not ego, within
+    // max_range + circumradius), each tested exactly only against the rays
+    // of a conservative angular interval around its bounding circle
+    for (int j = lane; j < A; j += 32) {
+      if (j == i || !svis[j]) continue;
+      const double cx = sx[j] - ox, cy = sy[j] - oy;
+      const double cr = scr[j];
+      if (!(hypot(cx, cy) <= max_range + cr)) continue;
+      const double dist = sqrt(cx * cx + cy * cy);
+      int k_lo = 0, k_hi = R - 1;
+      bool all = dist <= cr + 1e-3;
+      double rel = 0.0, half = 0.0;
+      if (!all) {
+        half = asin(fmin(1.0, (cr + 1e-3) / dist)) + 1e-6;
+        rel = atan2(cy, cx) - center;
+        rel -= kTwoPi * floor(rel / kTwoPi);           // [0, 2pi)
       }
-      if (bmin < best) {
-        best = bmin;
-        type = 0;
+      if (full_circle && !all) {
+        const double scl = (double)R / kTwoPi;
+        k_lo = (int)floor((rel - half) * scl - 1e-6);
+        k_hi = (int)ceil((rel + half) * scl + 1e-6);
+        if (k_hi - k_lo + 1 >= R) {
+          k_lo = 0;
+          k_hi = R - 1;
+        }
       }
+      if (!full_circle && !all && R > 1) {
+        // cone rays sit at rel angles -fov/2 + fov k/(R-1); try the interval
+        // around rel and around rel - 2pi (cone centred on 0)
+        const double scl = (double)(R - 1) / C.fov;
+        int lo = R, hi = -1;
+        for (int sh = 0; sh < 2; ++sh) {
+          const double rr = sh == 0 ? rel : rel - kTwoPi;
+          const int a = (int)floor((rr - half + 0.5 * C.fov) * scl - 1e-6);
+          const int b = (int)ceil((rr + half + 0.5 * C.fov) * scl + 1e-6);
+          const int a2 = a < 0 ? 0 : a, b2 = b > R - 1 ? R - 1 : b;
+          if (a2 <= b2) {
+            lo = min(lo, a2);
+            hi = max(hi, b2);
+          }
+        }
+        k_lo = lo;
+        k_hi = hi;
+      }
+      for (int m = k_lo; m <= k_hi; ++m) {
+        const int k = ((m % R) + R) % R;
+        const double d = ray_box(ox, oy, rdx[k], rdy[k], sx[j], sy[j], sc[j], ss[j], shl[j], shw[j]);
+        if (d != INFINITY)   // d >= 0; + 0.0 maps -0 to +0 so the bit order is the value order
+          atomicMin(&rbest[k], (unsigned long long)__double_as_longlong(d + 0.0));
+      }
+    }
+    __syncwarp();
+    for (int k = lane; k < R; k += 32) {
+      const double dx = rdx[k], dy = rdy[k];
+      double best = __longlong_as_double((long long)rbest[k]);
+      int type = best != INFINITY ? 0 : 3;
       bool edge = false;
       const double limit = fmin(best, max_range) * (1.0 + 1e-12) + 1e-9;
       const double smin = walk_segments(G, ox, oy, dx, dy, limit, edge);
@@ -286,8 +350,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
 }  // namespace
 
 size_t lidar_smem_bytes(int max_agents, int obs_width) {
-  return lidar_agents_bytes(max_agents) +
-         (size_t)kLidarWarps * ((obs_width + 3) & ~3) * sizeof(float);
+  const int n_rays = (obs_width - 7) / 5;
+  return lidar_agents_bytes(max_agents) + (size_t)kLidarWarps * lidar_warp_bytes(obs_width, n_rays);
 }
 
 int lidar_warps() { return kLidarWarps; }
