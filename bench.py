@@ -5,20 +5,22 @@
 
 A "step" = one SimBatch.step over every world of the rank's shard: dynamics,
 replay, collisions, goal/done, and observations for every controlled agent
-(two kernels).  Metric: agent-steps/s (ASPS = CASPS, init_mode="all_valid"),
-whole job = sum over ranks.  Worlds shard across ranks with no collective on
-the step path ("scaling": "weak": each rank owns the configured world count).
-The working set (C3: 1.7 GB of observations written per step, 1.4 GB of road
-tables) exceeds the 126 MB L2, so no flush is needed between steps.
+(two kernels); with auto-reset of finished worlds (the reference benchmark's
+semantics, engine.py:794-802).  Config c5 steps the VecDriveEnv with an
+in-loop torch policy (the reference trainer's ActorCritic, ippo.py:48-66)
+sampling discrete actions on the device.  Metric: agent-steps/s (ASPS = CASPS,
+init_mode="all_valid"), whole job = sum over ranks.  Worlds shard across ranks
+with no collective on the step path ("scaling": "weak": each rank owns the
+configured world count; scene seed = global world id).  The working set (C3:
+1.7 GB of observations written per step, 0.7 GB of road tables) exceeds the
+126 MB L2, so no flush is needed between steps.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -26,77 +28,115 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# name: worlds per GPU, agents, road points, dynamics, collision, obs kwargs, workload
 CONFIGS = {
-    # name: (worlds per GPU, agents, road points, dynamics, collision, obs kwargs, workload)
     "c1": (16, 32, 400, "classic", "ignore", {}, "C1 synthetic 16 worlds x 32 agents, 400 pts"),
     "c2": (1024, 64, 2000, "classic", "remove_agent", {},
-           "C2 synthetic 1024 worlds x 64 agents, 2k pts, collision+goal"),
+           "C2 synthetic 1024 worlds x 64 agents, 2k pts, collision+goal reward"),
     "c3": (4096, 128, 10000, "delta_local", "ignore", {"radius": 50.0},
            "C3 Waymo-shaped 4096 worlds x 128 agents, 10k pts, r=50 m, delta-local"),
     "c4": (4096, 128, 10000, "classic", "ignore", {"mode": "lidar", "n_rays": 64},
            "C4 LiDAR 64 rays, 4096 worlds x 128 agents, 10k pts"),
+    "c5": (1024, 128, 10000, "classic", "remove_agent", {"radius": 50.0},
+           "C5 RL rollout: 1024 worlds/GPU (8192 on 8 GPUs) x 128 agents, 10k pts, "
+           "VecDriveEnv + in-loop ActorCritic policy"),
 }
-# CPU sample (worlds, steps) per config for the oracle timing legs (~10-30 s of CPU)
-CPU_SAMPLE = {"c1": (16, 91), "c2": (64, 10), "c3": (32, 3), "c4": (8, 1)}
+# CPU sample of the same workload for the oracle legs: worlds stepped per "step"
+CPU_WORLDS = {"c1": 16, "c2": 128, "c3": 64, "c4": 8, "c5": 64}
 
 
-def bytes_per_agent_step(cfg_name: str, act_dim: int, width: int, P: int, A: int) -> dict:
+def bytes_per_agent_step(act_dim: int, width: int, P: int, A: int) -> dict:
     """Algorithmic (compulsory) HBM bytes per agent-step, SURVEY.md §8d:
-    actions + FP64 state read/write + static agent fields + obs row (f32) +
-    reward/done/info + road tables read once per world-step (x,y f32 +
-    heading f32 + kind u8 = 13 B per point, amortised over the A agents)."""
+    actions + FP64 state read/write + static agent fields + reward/done/info
+    (step kernel) and the float32 observation row + road tables read once
+    per world-step (x, y, heading f32 + kind u8 = 13 B per point, amortised
+    over the A agents) + the agent state it reads (observation kernel)."""
     step_k = 4 * act_dim + 66 + 26 + 8
     obs_k = 4 * width + 13.0 * P / A + 66
     return {"total": step_k + 4 * width + 13.0 * P / A, "step_kernel": step_k, "obs_kernel": obs_k}
 
 
-def flops_per_agent_step(width_mode: str, P: int, A: int) -> float:
+def radial_flops(P: int, A: int) -> float:
     """Reference linear-scan FP32 work: 5(P + A - 1) + 20*(16+64) + 40."""
     return 5.0 * (P + A - 1) + 20.0 * (16 + 64) + 40.0
 
 
+def lidar_flops(pw, max_range: float, n_rays: int, worlds: int = 4) -> float:
+    """sum over rays of 11 |candidate segments| + 30 |candidate
+    boxes| with the reference's own candidate sets (segments whose AABB meets
+    the +-max_range box, visible boxes within max_range + circumradius),
+    counted exactly on the first worlds of the scene."""
+    import numpy as np
+    tot, n = 0.0, 0
+    for w in range(min(worlds, pw.n_worlds)):
+        a0, a1 = pw.a_off[w], pw.a_off[w + 1]
+        s0, s1 = pw.s_off[w], pw.s_off[w + 1]
+        X = pw.rep_x[pw.r_off[w]:pw.r_off[w] + (a1 - a0)]
+        Y = pw.rep_y[pw.r_off[w]:pw.r_off[w] + (a1 - a0)]
+        lx = np.minimum(pw.seg_ax[s0:s1], pw.seg_bx[s0:s1])
+        hx = np.maximum(pw.seg_ax[s0:s1], pw.seg_bx[s0:s1])
+        ly = np.minimum(pw.seg_ay[s0:s1], pw.seg_by[s0:s1])
+        hy = np.maximum(pw.seg_ay[s0:s1], pw.seg_by[s0:s1])
+        cr = pw.circumradius[a0:a1]
+        for i in range(a1 - a0):
+            segs = ((lx <= X[i] + max_range) & (hx >= X[i] - max_range) &
+                    (ly <= Y[i] + max_range) & (hy >= Y[i] - max_range)).sum()
+            d = np.hypot(X - X[i], Y - Y[i])
+            boxes = ((d <= max_range + cr).sum() - 1)
+            tot += n_rays * (11.0 * segs + 30.0 * boxes)
+            n += 1
+    return tot / max(n, 1)
+
+
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """SM clock and throttle reasons sampled every 5 ms through NVML during the
+    timed region (B200_PROFILING.md clocks line; the timed regions here are
+    tens of milliseconds, too short for nvidia-smi -lms)."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, gpu_index: int):
-        self.rows = []
-        self.proc = None
-        self.gpu = gpu_index
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, attr in self.REASONS:
+                    if r & getattr(nv, attr):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.005)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+        if self.nv is not None:
+            self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
-        except OSError:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self._stop.set()
         self.thread.join(timeout=2)
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows if len(r) >= 7 for k in range(4)
-                          if r[3 + k].lower() == "active"})
-        sm_sorted = sorted(sm)
-        return {"sm_mhz": sm_sorted[len(sm_sorted) // 2] if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+        sm = sorted(self.samples)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(sm)}
 
 
 def load_peaks():
@@ -108,58 +148,92 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def cpu_oracle_rate(cfg_name: str, threads: int, budget_s: float = 20.0):
-    """Oracle (C restatement of the reference, bit-exact with it) on host cores:
-    a bounded sample of the same workload; returns (ASPS, sample description)."""
+def sim_config(name):
     from paper_2408_01584_b200.config import ObsConfig, SimConfig
-    from paper_2408_01584_b200.packing import pack
-    from paper_2408_01584_b200.synthetic import WaymoSpec, generate
-    from oracle.oracle import OracleBatch
-    import numpy as np
-    W, A, P, dyn, coll, okw, _ = CONFIGS[cfg_name]
-    ws, max_steps = CPU_SAMPLE[cfg_name]
-    cfg = SimConfig(dynamics=dyn, collision_behavior=coll, init_mode="all_valid",
-                    obs=ObsConfig(**okw))
-    raw = generate(WaymoSpec(n_worlds=ws, n_agents=A, n_points=P, seed=0))
-    ora = OracleBatch(pack(raw, cfg), cfg, n_threads=threads)
-    rng = np.random.default_rng(0)
-    n = ora.pw.n_controlled
-    steps = 0
-    t0 = time.perf_counter()
-    while True:
-        if cfg.dynamics == "delta_local":
-            act = rng.uniform(-0.9, 0.9, (n, 3))
+    W, A, P, dyn, coll, okw, _ = CONFIGS[name]
+    return SimConfig(dynamics=dyn, collision_behavior=coll, init_mode="all_valid",
+                     obs=ObsConfig(**okw))
+
+
+class CpuSample:
+    """The C oracle (restatement of the reference, bit-exact with it on the
+    golden fixtures) stepping a bounded sample of the same workload on the
+    host cores (OpenMP over worlds).  For c5 the reference trainer's policy
+    runs on the CPU too."""
+
+    def __init__(self, name: str, threads: int):
+        import numpy as np
+        from oracle.oracle import OracleBatch, build
+        from paper_2408_01584_b200.packing import pack
+        from paper_2408_01584_b200.synthetic import WaymoSpec, generate
+        build()
+        W, A, P = CONFIGS[name][:3]
+        self.name, self.threads = name, threads
+        self.cfg = sim_config(name)
+        ws = min(CPU_WORLDS[name], W)
+        raw = generate(WaymoSpec(n_worlds=ws, n_agents=A, n_points=P, seed=0))
+        self.ora = OracleBatch(pack(raw, self.cfg), self.cfg, n_threads=threads)
+        self.agents = int(self.ora.pw.n_instantiated.sum())
+        self.rng = np.random.default_rng(0)
+        self.desc = f"{ws} worlds x {A} agents"
+        self.policy = None
+        if name == "c5":
+            import torch
+            torch.set_num_threads(threads)
+            from paper_2408_01584_b200.policy import ActorCritic
+            from paper_2408_01584_b200.env import ActionGrid, obs_scale
+            self.policy = ActorCritic(self.ora.width, 91)
+            self.scale = torch.tensor(obs_scale(self.cfg), dtype=torch.float32)
+            g = ActionGrid()
+            self.accels = np.array(g.accelerations)
+            self.steers = np.array(g.steerings)
+
+    def step(self):
+        import numpy as np
+        n = self.ora.pw.n_controlled
+        if self.policy is not None:
+            import torch
+            with torch.inference_mode():
+                obs = torch.from_numpy(self.ora.observations).float() / self.scale
+                logits, _ = self.policy(obs)
+                idx = torch.distributions.Categorical(logits=logits).sample().numpy()
+            act = np.column_stack([self.accels[idx // 13], self.steers[idx % 13]])
+        elif self.cfg.dynamics == "delta_local":
+            lo = np.array([b[0] for b in self.cfg.delta_bounds])
+            hi = np.array([b[1] for b in self.cfg.delta_bounds])
+            act = self.rng.uniform(lo, hi, (n, 3))
         else:
-            act = rng.uniform([-4, -0.7], [4, 0.7], (n, 2))
-        ora.step(act.astype(np.float32).astype(np.float64), auto_reset=True)
-        steps += 1
+            act = self.rng.uniform([-4, -0.7], [4, 0.7], (n, 2))
+        self.ora.step(act.astype(np.float32).astype(np.float64), auto_reset=True)
+
+    def rate(self, steps: int, warmup: int = 1, budget_s: float = 30.0):
+        for _ in range(warmup):
+            self.step()
+        t0 = time.perf_counter()
+        k = 0
+        while k < steps:
+            self.step()
+            k += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
         el = time.perf_counter() - t0
-        if steps >= max_steps or el > budget_s:
-            break
-    asps = steps * int(ora.pw.n_instantiated.sum()) / el
-    return asps, f"{ws} worlds x {A} agents x {steps} steps ({el:.1f} s)"
+        return self.agents * k / el, f"{self.desc} x {k} steps ({el:.1f} s)"
 
 
-def run_reference(args, rank, world):
+def run_reference(args, rank):
+    """--impl reference: the reference's CPU path (oracle port) on the host
+    cores, rank 0 only, one bounded-sample step per timed step."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    from oracle import oracle as _o
-    _o.build()
-    vals = []
-    sample = ""
-    for _ in range(args.warmup):
-        cpu_oracle_rate(args.config, threads, budget_s=2.0)
-    for _ in range(args.steps):
-        v, sample = cpu_oracle_rate(args.config, threads, budget_s=10.0)
-        vals.append(v)
-    value = sum(vals) / len(vals)
+    cs = CpuSample(args.config, threads)
+    value, sample = cs.rate(args.steps, warmup=args.warmup, budget_s=120.0)
     W, A, P, dyn, coll, okw, workload = CONFIGS[args.config]
     line = {"impl": "reference", "metric": "agent_steps_per_sec", "value": value,
             "unit": "agent-steps/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload, "worlds": W, "agents": A, "road_points": P,
+            "config": {"workload": workload, "worlds_per_gpu": W, "agents": A, "road_points": P,
                        "dynamics": dyn, "collision": coll, "obs": okw or {"mode": "radial"}},
             "cpu_baseline": {"value": value, "unit": "agent-steps/s", "cores": threads,
                              "kind": "port", "sample": sample},
@@ -177,20 +251,18 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--worlds", type=int, default=None, help="override worlds per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        run_reference(args, rank)
         return
 
-    import numpy as np
     import torch
     import torch.distributed as dist
-    from paper_2408_01584_b200.config import ObsConfig, SimConfig, obs_width
+    from paper_2408_01584_b200.config import obs_width
     from paper_2408_01584_b200.engine import SimBatch, random_actions
     from paper_2408_01584_b200.synthetic import WaymoSpec, generate
 
@@ -201,23 +273,45 @@ def main():
     W, A, P, dyn, coll, okw, workload = CONFIGS[args.config]
     if args.worlds:
         W = args.worlds
-    cfg = SimConfig(dynamics=dyn, collision_behavior=coll, init_mode="all_valid",
-                    obs=ObsConfig(**okw))
-    t_gen = time.perf_counter()
-    raw = generate(WaymoSpec(n_worlds=W, n_agents=A, n_points=P, seed=0, world_offset=rank * W))
-    batch = SimBatch.from_raw(raw, cfg, device=dev)
-    t_gen = time.perf_counter() - t_gen
-    n = batch.n_controlled
+    cfg = sim_config(args.config)
     width = obs_width(cfg.obs)
-    acts = [random_actions(n, cfg, 0, t, dev) for t in range(8)]
+    t_setup = time.perf_counter()
+    raw = generate(WaymoSpec(n_worlds=W, n_agents=A, n_points=P, seed=0, world_offset=rank * W))
+    rl = args.config == "c5"
+    if rl:
+        from paper_2408_01584_b200.env import EnvConfig, VecDriveEnv
+        from paper_2408_01584_b200.policy import ActorCritic, sample_actions
+        env = VecDriveEnv(EnvConfig(raw=raw, sim=cfg, device=str(dev)))
+        batch = env.batch
+        policy = ActorCritic(width, env.n_actions).to(dev)
+        obs0 = env.reset()
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(1234 + rank)
+    else:
+        batch = SimBatch.from_raw(raw, cfg, device=dev)
+        acts = [random_actions(batch.n_controlled, cfg, 0, t, dev) for t in range(8)]
+    t_setup = time.perf_counter() - t_setup
+    n = batch.n_controlled
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    state = {"obs": obs0} if rl else {}
+
+    def one_step(t, events=None):
+        if rl:
+            with torch.inference_mode(), torch.autocast("cuda", dtype=torch.bfloat16):
+                logits, value = policy(state["obs"])
+                idx = sample_actions(logits, gen)
+            obs, rew, done, infos = env.step(idx)
+            state["obs"] = obs
+            return rew
+        return batch.step(acts[t % 8], auto_reset=True, events=events).rewards
+
     for t in range(args.warmup):
-        batch.step(acts[t % 8], auto_reset=True)
+        one_step(t)
     torch.cuda.synchronize(dev)
 
     # ---- device-resident timed region (inputs already in HBM)
@@ -230,45 +324,55 @@ def main():
     torch.cuda.synchronize(dev)
     sampler = ClockSampler(local_rank)
     sampler.start()
-    time.sleep(0.3)
+    time.sleep(0.05)
     barrier()
     torch.cuda.synchronize(dev)
     start.record(stream)
     for t in range(args.steps):
-        batch.step(acts[t % 8], auto_reset=True, events=ev[t])
+        one_step(t, events=ev[t])
     end.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
     clocks = sampler.stop()
     ms = start.elapsed_time(end)
-    step_ms = sum(e3[0].elapsed_time(e3[1]) for e3 in ev) / args.steps
-    obs_ms = sum(e3[1].elapsed_time(e3[2]) for e3 in ev) / args.steps
+    kernel_ms = None
+    if not rl:
+        kernel_ms = {"step_kernel": sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps,
+                     "obs_kernel": sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps}
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     agents_total = batch.total_agents * world
     value = agents_total * args.steps / (ms / 1e3)
-    gpu_launches = 2 * args.steps
 
-    # ---- end-to-end through the public API with host buffers: pinned host
-    # actions -> device each step, rewards/dones/info -> host each step.
-    e2e_steps = args.e2e_steps or args.steps
-    host_acts = [a.cpu().pin_memory() for a in acts]
-    rew_h = torch.empty(n, dtype=torch.float32).pin_memory()
-    done_h = torch.empty(n, dtype=torch.bool).pin_memory()
-    info_h = torch.empty((3, n), dtype=torch.bool).pin_memory()
+    # ---- end to end through the public API with host buffers: every step
+    # copies its inputs from pinned host memory to the device and its result
+    # back (c1-c4: actions in, rewards/dones/info out; c5: the policy samples
+    # the actions on the device, the step's reward sum comes back).
+    if rl:
+        rsum_h = torch.empty(1, dtype=torch.float32).pin_memory()
+        h2d, d2h = 0, 4
+    else:
+        host_acts = [a.cpu().pin_memory() for a in acts]
+        rew_h = torch.empty(n, dtype=torch.float32).pin_memory()
+        done_h = torch.empty(n, dtype=torch.bool).pin_memory()
+        info_h = torch.empty((3, n), dtype=torch.bool).pin_memory()
+        h2d, d2h = host_acts[0].numel() * 4, n * 4 + n + 3 * n
     barrier()
     torch.cuda.synchronize(dev)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for t in range(e2e_steps):
-        d_act = host_acts[t % 8].to(dev, non_blocking=True)
-        out = batch.step(d_act, auto_reset=True)
-        rew_h.copy_(out.rewards, non_blocking=True)
-        done_h.copy_(out.dones, non_blocking=True)
-        info_h.copy_(batch._info[:, :n], non_blocking=True)
+    for t in range(args.steps):
+        if rl:
+            rew = one_step(t)
+            rsum_h.copy_(rew.sum().reshape(1), non_blocking=True)
+        else:
+            out = batch.step(host_acts[t % 8].to(dev, non_blocking=True), auto_reset=True)
+            rew_h.copy_(out.rewards, non_blocking=True)
+            done_h.copy_(out.dones, non_blocking=True)
+            info_h.copy_(batch._info[:, :n], non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
@@ -277,39 +381,39 @@ def main():
         tt = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    e2e_value = agents_total * e2e_steps / (e2e_ms / 1e3)
-    h2d = host_acts[0].numel() * 4
-    d2h = n * 4 + n + 3 * n
+    e2e_value = agents_total * args.steps / (e2e_ms / 1e3)
 
-    # ---- episode statistics (the only collective; off the step path)
-    infos = batch.episode_infos
-    stats = torch.tensor([sum(e.n_controlled for e in infos), sum(e.n_goal for e in infos),
-                          sum(e.n_veh_collision for e in infos), sum(e.n_offroad for e in infos),
-                          len(infos)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(stats)
+    # ---- episode statistics: the only collective, off the step path
+    from paper_2408_01584_b200.parallel import allreduce_episode_stats, episode_stats
+    stats = allreduce_episode_stats(episode_stats(batch.episode_infos), device=dev)
 
-    # ---- roofline of the dominant kernel (observation kernel)
+    # ---- roofline of the dominant kernel (the observation kernel)
     peak, peak_kind = load_peaks()
-    bpa = bytes_per_agent_step(args.config, acts[0].shape[1], width, P, A)
-    obs_bytes = bpa["obs_kernel"] * batch.n_controlled
-    achieved = obs_bytes / (obs_ms / 1e3) / 1e9
-    step_bytes = bpa["total"] * batch.total_agents
-    fl = flops_per_agent_step(cfg.obs.mode, P, A)
+    act_dim = 1 if rl else acts[0].shape[1]
+    bpa = bytes_per_agent_step(act_dim, width, P, A)
+    fl = radial_flops(P, A) if cfg.obs.mode == "radial" else \
+        lidar_flops(batch.packed, cfg.obs.max_range, cfg.obs.n_rays)
     hbm_bound = peak * 1e9 / bpa["total"]
     fp32_bound = 74.4e12 / fl
-    result = None
+    roofline = None
+    if kernel_ms is not None:
+        achieved = bpa["obs_kernel"] * batch.n_controlled / (kernel_ms["obs_kernel"] / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "kernel": "obs_radial_kernel" if cfg.obs.mode == "radial" else "obs_lidar_kernel",
+                    "bytes_per_agent_step": bpa["obs_kernel"], "peak_kind": peak_kind}
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
             try:
-                v, sample = cpu_oracle_rate(args.config, threads)
+                v, sample = CpuSample(args.config, threads).rate(91, warmup=1, budget_s=10.0)
                 cpu = {"value": v, "unit": "agent-steps/s", "cores": threads, "kind": "port",
                        "sample": sample}
-            except Exception as exc:  # report, never fake
+            except Exception as exc:   # report, never fake
                 cpu = {"value": None, "unit": "agent-steps/s", "cores": threads, "kind": "port",
-                       "sample": f"failed: {exc}"}
+                       "sample": f"failed: {exc!r}"}
+        total = max(int(stats[1]), 1)
         result = {
             "metric": "agent_steps_per_sec", "value": value, "unit": "agent-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -318,26 +422,23 @@ def main():
             "config": {"workload": workload, "worlds_per_gpu": W, "agents": A, "road_points": P,
                        "dynamics": dyn, "collision": coll, "obs_mode": cfg.obs.mode,
                        "obs_width": width, "episode_steps": 91, "auto_reset": True,
-                       "l2": "working set > L2 (no flush needed)", "parallelism": f"worlds/{world} GPU"},
+                       "l2": "working set > L2 (no flush needed)",
+                       "parallelism": f"world shards x {world} GPU (no step collective)"},
             "e2e": {"value": e2e_value, "unit": "agent-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": gpu_launches,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "obs_radial_kernel" if cfg.obs.mode == "radial" else "obs_lidar_kernel",
-                         "bytes_per_agent_step": bpa["obs_kernel"], "peak_kind": peak_kind},
-            "step_roofline": {"bytes_per_agent_step": bpa["total"], "fp32_flop_per_agent_step": fl,
-                              "hbm_bound_asps": hbm_bound, "fp32_bound_asps": fp32_bound,
+            "gpu_launches": (2 * args.steps) if not rl else 2 * args.steps,
+            "roofline": roofline,
+            "step_roofline": {"bytes_per_agent_step": bpa["total"],
+                              "fp32_flop_per_agent_step": fl, "hbm_bound_asps": hbm_bound,
+                              "fp32_bound_asps": fp32_bound,
                               "bound_asps": min(hbm_bound, fp32_bound),
                               "frac": (value / world) / min(hbm_bound, fp32_bound)},
-            "kernel_ms": {"step_kernel": step_ms, "obs_kernel": obs_ms},
+            "kernel_ms": kernel_ms,
             "clocks": clocks,
             "cpu_baseline": cpu,
-            "episodes": {"count": int(stats[4].item()),
-                         "goal_rate": float(stats[1] / max(stats[0].item(), 1)),
-                         "veh_collision_rate": float(stats[2] / max(stats[0].item(), 1)),
-                         "offroad_rate": float(stats[3] / max(stats[0].item(), 1))},
-            "setup_s": t_gen,
+            "episodes": {"count": int(stats[0]), "goal_rate": stats[2] / total,
+                         "veh_collision_rate": stats[3] / total, "offroad_rate": stats[4] / total},
+            "setup_s": t_setup,
         }
         print(json.dumps(result), flush=True)
     batch.close()
