@@ -139,6 +139,16 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(sm)}
 
 
+def load_traffic(config: str, kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/r1_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            return json.load(f)[config][kernel]
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -398,9 +408,13 @@ def main():
     roofline = None
     if kernel_ms is not None:
         achieved = bpa["obs_kernel"] * batch.n_controlled / (kernel_ms["obs_kernel"] / 1e3) / 1e9
+        kname = "obs_radial_kernel" if cfg.obs.mode == "radial" else "obs_lidar_kernel"
+        tr = load_traffic(args.config, kname) if (args.worlds or W) == CONFIGS[args.config][0] else None
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": None,
-                    "kernel": "obs_radial_kernel" if cfg.obs.mode == "radial" else "obs_lidar_kernel",
+                    "frac": achieved / peak, "traffic": tr / 1e9 if tr else None,
+                    "traffic_unit": "GB per launch (ncu dram__bytes_read+write)",
+                    "algorithmic_gb_per_launch": bpa["obs_kernel"] * batch.n_controlled / 1e9,
+                    "kernel": kname,
                     "bytes_per_agent_step": bpa["obs_kernel"], "peak_kind": peak_kind}
     if rank == 0:
         cpu = None

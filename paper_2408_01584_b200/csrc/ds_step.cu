@@ -17,7 +17,7 @@
 namespace ds {
 
 struct StepShared {
-  double *x, *y, *c, *s, *hl, *hw;
+  double *x, *y, *c, *s, *hl, *hw, *cr;
   uint8_t *elig;
 };
 
@@ -30,12 +30,13 @@ __device__ __forceinline__ StepShared carve_step(void *base, int amax) {
   sh.s = d + 3 * amax;
   sh.hl = d + 4 * amax;
   sh.hw = d + 5 * amax;
-  sh.elig = reinterpret_cast<uint8_t *>(d + 6 * amax);
+  sh.cr = d + 6 * amax;
+  sh.elig = reinterpret_cast<uint8_t *>(d + 7 * amax);
   return sh;
 }
 
 size_t step_smem_bytes(int max_agents) {
-  return (size_t)max_agents * (6 * sizeof(double) + 1) + 16;
+  return (size_t)max_agents * (7 * sizeof(double) + 1) + 16;
 }
 
 // SAT over the 4 box axes, _fastpath.sat_pairs (fp:29-53); (i, j) with i < j.
@@ -117,9 +118,12 @@ __device__ bool offroad_query(const ds_tables &T, const ds_config &C, int w, dou
       const int64_t cell = cbase + (int64_t)iy * nx + ix;
       const int b = T.eseg_cell_start[cell], e = T.eseg_cell_start[cell + 1];
       for (int k = b; k < e; ++k) {
-        if (seg_box_hit(cx, cy, ck, sk, hl, hw, T.eseg_ax[k], T.eseg_ay[k], T.eseg_bx[k],
-                        T.eseg_by[k]))
-          return true;
+        const double ax = T.eseg_ax[k], ay = T.eseg_ay[k], bx = T.eseg_bx[k], by = T.eseg_by[k];
+        // segment AABB vs box AABB (with slack): a superset prefilter
+        if (fmax(ax, bx) < cx - rx || fmin(ax, bx) > cx + rx || fmax(ay, by) < cy - ry ||
+            fmin(ay, by) > cy + ry)
+          continue;
+        if (seg_box_hit(cx, cy, ck, sk, hl, hw, ax, ay, bx, by)) return true;
       }
     }
   }
@@ -271,6 +275,7 @@ __global__ void __launch_bounds__(1024) step_kernel(ds_tables T, ds_config C, ds
     sh.s[tid] = sin(h);
     sh.hl[tid] = T.half_l[g];
     sh.hw[tid] = T.half_w[g];
+    sh.cr[tid] = T.circumradius[g];
     const bool elig = (f & DS_F_PRESENT) && !(f & DS_F_REMOVED) &&
                       ((ctrl && !(f & DS_F_DONE)) || T.rep_valid[rn]);
     sh.elig[tid] = elig;
@@ -279,8 +284,12 @@ __global__ void __launch_bounds__(1024) step_kernel(ds_tables T, ds_config C, ds
 
   bool collided = false, offroad = false;
   if (act_here && sh.elig[tid]) {
+    const double xi = sh.x[tid], yi = sh.y[tid], cri = sh.cr[tid];
     for (int j = 0; j < A; ++j) {
       if (j == tid || !sh.elig[j]) continue;
+      // boxes lie inside their circumcircles: disjoint circles cannot collide
+      const double dx = sh.x[j] - xi, dy = sh.y[j] - yi, rr = cri + sh.cr[j];
+      if (dx * dx + dy * dy > rr * rr * (1.0 + 1e-9) + 1e-9) continue;
       if (j > tid ? sat_hit(sh, tid, j) : sat_hit(sh, j, tid)) {
         collided = true;
         break;
