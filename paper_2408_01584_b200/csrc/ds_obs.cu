@@ -31,7 +31,8 @@ namespace ds {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNB = 256;       // histogram buckets
-constexpr int kCand = 640;     // buffered pass-1 candidates (global-points variant)
+constexpr int kCandGlobal = 640;  // buffered pass-1 candidates (global-points variant)
+constexpr int kCandShared = 224;  // (shared-points variant: hint-narrowed scans)
 constexpr int kWarpsShared = 20;
 constexpr int kWarpsGlobal = 12;
 
@@ -60,8 +61,9 @@ __host__ __device__ inline WarpLayout warp_layout(const ds_config &c, bool buffe
   size_t o = al16(head);
   L.row = o - head;
   L.hc = o; o = al16(o + kNB * sizeof(uint32_t));
-  L.ca = o; if (buffered) o = al16(o + kCand * sizeof(float));
-  L.cp = o; if (buffered) o = al16(o + kCand * sizeof(uint16_t));
+  const int cc = buffered ? kCandGlobal : kCandShared;
+  L.ca = o; o = al16(o + cc * sizeof(float));
+  L.cp = o; o = al16(o + cc * sizeof(uint16_t));
   L.ga = o; o = al16(o + gc * sizeof(float));
   L.ge = o; o = al16(o + gc * sizeof(double));
   L.gid = o; o = al16(o + gc * sizeof(int));
@@ -98,7 +100,7 @@ struct Sel {
   int *gid, *gpl;
   uint8_t *gb, *gf;
   int *sel_pl, *sel_id;
-  int gcap;
+  int gcap, ccap;
 };
 
 __device__ __forceinline__ bool key_less(double da, int ia, double db, int ib) {
@@ -382,7 +384,96 @@ __device__ __forceinline__ double hint_radius(double hint, double radius, double
   return fmin(sqrt(hint * hint + 3.1 * w + D) + 1e-3, radius);
 }
 
-template <bool Buffered, class Src>
+// Rank the set G[0, n_g) (bucket-sorted, counting-sort cursors in S.hc) with
+// the float keys; near ties and possibly-out-of-radius keys get the exact
+// (distance, id) treatment.  Returns min(#valid, k); payloads in S.sel_pl.
+template <class Src>
+__device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float beta, float two_d,
+                        double r2, double D, double radius, int k, const Sel &S, int lane) {
+  // phase A: rank by float key; flag near ties and possibly-out-of-radius keys
+  int flagged = 0;
+  for (int p = lane; p < n_g; p += 32) {
+    const float ap = S.ga[p];
+    const int b = S.gb[p];
+    const float t = ap * inv_w;
+    const float fr = t - floorf(t);
+    const bool edge = fr < beta || fr > 1.0f - beta;
+    const int lo = edge ? (b > 0 ? b - 1 : 0) : b;
+    const int hi = edge ? (b < bmax ? b + 1 : bmax) : b;
+    const uint32_t hlo = S.hc[lo], hhi = S.hc[hi];
+    const int start = (int)(hlo >> 16) - (int)(hlo & 0xffffu);
+    const int end = (int)(hhi >> 16);
+    const float dlo = ap - two_d, dhi = ap + two_d;
+    int rank = start;
+    bool amb = false;
+    for (int q = start; q < end; ++q) {
+      if (q == p) continue;
+      const float aq = S.ga[q];
+      rank += aq < dlo ? 1 : 0;
+      amb |= aq >= dlo && aq <= dhi;
+    }
+    const uint8_t f = (amb ? 1 : 0) | ((double)ap > r2 - D ? 2 : 0) | (edge ? 8 : 0);
+    S.gf[p] = f;
+    if (!(f & 3) && rank < k) S.sel_pl[rank] = S.gpl[p];
+    flagged += (f & 3) != 0;
+  }
+  int n_invalid = 0;
+  if (__any_sync(kFull, flagged)) {
+    __syncwarp();
+    // phase B: exact (distance, id) of the flagged elements
+    for (int p = lane; p < n_g; p += 32) {
+      const uint8_t f = S.gf[p];
+      if (!(f & 3)) continue;
+      int id;
+      const double e = src.exact(S.gpl[p], id);
+      S.ge[p] = e;
+      S.gid[p] = id;
+      if (e > radius) {
+        S.gf[p] = f | 4;
+        ++n_invalid;
+      }
+    }
+    __syncwarp();
+    // phase C: rank the valid flagged elements (near ties compared exactly;
+    // ambiguity is symmetric, so both ends of a near tie carry exact keys)
+    for (int p = lane; p < n_g; p += 32) {
+      const uint8_t f = S.gf[p];
+      if (!(f & 3) || (f & 4)) continue;
+      const float ap = S.ga[p];
+      const int b = S.gb[p];
+      const bool edge = f & 8;
+      const int lo = edge ? (b > 0 ? b - 1 : 0) : b;
+      const int hi = edge ? (b < bmax ? b + 1 : bmax) : b;
+      const uint32_t hlo = S.hc[lo], hhi = S.hc[hi];
+      const int start = (int)(hlo >> 16) - (int)(hlo & 0xffffu);
+      const int end = (int)(hhi >> 16);
+      const float dlo = ap - two_d, dhi = ap + two_d;
+      const double ep = S.ge[p];
+      const int ip = S.gid[p];
+      int rank = start;
+      for (int q = start; q < end; ++q) {
+        if (q == p) continue;
+        const float aq = S.ga[q];
+        if (aq < dlo) {
+          ++rank;
+        } else if (aq <= dhi) {
+          if (!(S.gf[q] & 4) && key_less(S.ge[q], S.gid[q], ep, ip)) ++rank;
+        }
+      }
+      if (rank < k) S.sel_pl[rank] = S.gpl[p];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) n_invalid += __shfl_xor_sync(kFull, n_invalid, off);
+  }
+  __syncwarp();
+  const int n_valid = n_g - n_invalid;
+  return n_valid < k ? n_valid : k;
+}
+
+// Exact ascending top-min(n_valid, k) by (distance, id).  Direct: small
+// candidate sets (partners) are compacted straight into G and ranked as one
+// bucket; a larger set takes the histogram path.
+template <bool Direct, class Src>
 __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S, int lane,
                            double rho, float &bound_out) {
   if (k <= 0) return 0;
@@ -395,8 +486,31 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
   if (!(beta < 0.125f)) return select_serial(src, k, radius, r2hi, S, lane);
   // near-tie band in float, padded by the float rounding of a - 2D
   const float two_d = (float)(2.0 * D + 2.5e-7 * (double)r2hi);
+  if (Direct) {
+    int n = 0;
+    src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
+      const unsigned bal = __ballot_sync(kFull, ok);
+      const int pos = n + __popc(bal & ((1u << lane) - 1u));
+      if (ok && pos < S.gcap) {
+        S.ga[pos] = a;
+        S.gpl[pos] = pl;
+        S.gb[pos] = 0;
+      }
+      n += __popc(bal);
+    });
+    bound_out = 0.0f;
+    if (n == 0) return 0;
+    if (n <= S.gcap && n <= 0xffff) {
+      if (lane == 0) S.hc[0] = ((uint32_t)n << 16) | (uint32_t)n;
+      __syncwarp();
+      // one bucket: inv_w = 0 puts every key on the bucket "edge" -> window 0..0
+      return rank_set(src, n, 0, 0.0f, beta, two_d, r2, D, radius, k, S, lane);
+    }
+    __syncwarp();
+  }
   bool restricted = rho < radius;
   const int pb = src.pbase();
+  const bool small = src.small_payload();
   constexpr int kPer = kNB / 32;
   uint32_t total, n_g, incl, local;
   uint32_t cnt[kPer];
@@ -407,15 +521,13 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     nbuf = 0;
     src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
       if (ok) atomicAdd(&S.hc[bucket_of(a, inv_w)], 1u);
-      if (Buffered) {
-        const unsigned bal = __ballot_sync(kFull, ok);
-        const int pos = nbuf + __popc(bal & ((1u << lane) - 1u));
-        if (ok && pos < kCand) {
-          S.ca[pos] = a;
-          S.cp[pos] = (uint16_t)(pl - pb);
-        }
-        nbuf += __popc(bal);
+      const unsigned bal = __ballot_sync(kFull, ok);
+      const int pos = nbuf + __popc(bal & ((1u << lane) - 1u));
+      if (ok && pos < S.ccap) {
+        S.ca[pos] = a;
+        S.cp[pos] = (uint16_t)(pl - pb);
       }
+      nbuf += __popc(bal);
     });
     __syncwarp();
     local = 0;
@@ -441,7 +553,7 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) bstar = min(bstar, __shfl_xor_sync(kFull, bstar, off));
     bmax = min(bstar + 2, kNB - 1);
-    // restricted scan valid only if all buckets <= bmax lie inside the disc
+    // a narrowed scan is valid only if all buckets <= bmax lie inside the disc
     if (restricted && !((((double)bmax + 1.01) * w + D) <= rho * rho)) {
       src.restrict_to(radius + 1e-6, lane);
       restricted = false;
@@ -478,7 +590,7 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
       S.gb[pos] = (uint8_t)b;
     }
   };
-  if (Buffered && nbuf <= kCand && src.small_payload()) {
+  if (nbuf <= S.ccap && small) {
     for (int p = lane; p < nbuf; p += 32) scatter(S.ca[p], pb + (int)S.cp[p]);
   } else {
     // only keys in buckets <= bmax matter: a < (bmax + 1) w, so d^2 < that + D
@@ -488,84 +600,7 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     });
   }
   __syncwarp();
-  // phase A: rank by float key; flag near ties and possibly-out-of-radius keys
-  int flagged = 0;
-  for (int p = lane; p < (int)n_g; p += 32) {
-    const float ap = S.ga[p];
-    const int b = S.gb[p];
-    const float t = ap * inv_w;
-    const float fr = t - floorf(t);
-    const bool edge = fr < beta || fr > 1.0f - beta;
-    const int lo = edge ? (b > 0 ? b - 1 : 0) : b;
-    const int hi = edge ? (b < bmax ? b + 1 : bmax) : b;
-    const uint32_t hlo = S.hc[lo], hhi = S.hc[hi];
-    const int start = (int)(hlo >> 16) - (int)(hlo & 0xffffu);
-    const int end = (int)(hhi >> 16);
-    const float dlo = ap - two_d, dhi = ap + two_d;
-    int rank = start;
-    bool amb = false;
-    for (int q = start; q < end; ++q) {
-      if (q == p) continue;
-      const float aq = S.ga[q];
-      rank += aq < dlo ? 1 : 0;
-      amb |= aq >= dlo && aq <= dhi;
-    }
-    const uint8_t f = (amb ? 1 : 0) | ((double)ap > r2 - D ? 2 : 0) | (edge ? 8 : 0);
-    S.gf[p] = f;
-    if (!(f & 3) && rank < k) S.sel_pl[rank] = S.gpl[p];
-    flagged += (f & 3) != 0;
-  }
-  int n_invalid = 0;
-  if (__any_sync(kFull, flagged)) {
-    __syncwarp();
-    // phase B: exact (distance, id) of the flagged elements
-    for (int p = lane; p < (int)n_g; p += 32) {
-      const uint8_t f = S.gf[p];
-      if (!(f & 3)) continue;
-      int id;
-      const double e = src.exact(S.gpl[p], id);
-      S.ge[p] = e;
-      S.gid[p] = id;
-      if (e > radius) {
-        S.gf[p] = f | 4;
-        ++n_invalid;
-      }
-    }
-    __syncwarp();
-    // phase C: rank the valid flagged elements (near ties compared exactly;
-    // ambiguity is symmetric, so both ends of a near tie carry exact keys)
-    for (int p = lane; p < (int)n_g; p += 32) {
-      const uint8_t f = S.gf[p];
-      if (!(f & 3) || (f & 4)) continue;
-      const float ap = S.ga[p];
-      const int b = S.gb[p];
-      const bool edge = f & 8;
-      const int lo = edge ? (b > 0 ? b - 1 : 0) : b;
-      const int hi = edge ? (b < bmax ? b + 1 : bmax) : b;
-      const uint32_t hlo = S.hc[lo], hhi = S.hc[hi];
-      const int start = (int)(hlo >> 16) - (int)(hlo & 0xffffu);
-      const int end = (int)(hhi >> 16);
-      const float dlo = ap - two_d, dhi = ap + two_d;
-      const double ep = S.ge[p];
-      const int ip = S.gid[p];
-      int rank = start;
-      for (int q = start; q < end; ++q) {
-        if (q == p) continue;
-        const float aq = S.ga[q];
-        if (aq < dlo) {
-          ++rank;
-        } else if (aq <= dhi) {
-          if (!(S.gf[q] & 4) && key_less(S.ge[q], S.gid[q], ep, ip)) ++rank;
-        }
-      }
-      if (rank < k) S.sel_pl[rank] = S.gpl[p];
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) n_invalid += __shfl_xor_sync(kFull, n_invalid, off);
-  }
-  __syncwarp();
-  const int n_valid = (int)n_g - n_invalid;
-  return n_valid < k ? n_valid : k;
+  return rank_set(src, (int)n_g, bmax, inv_w, beta, two_d, r2, D, radius, k, S, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -607,6 +642,7 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
   S.sel_pl = reinterpret_cast<int *>(wb + WL.sel_pl);
   S.sel_id = reinterpret_cast<int *>(wb + WL.sel_id);
   S.gcap = gcap_of(C);
+  S.ccap = SharedPts ? kCandShared : kCandGlobal;
   float *row = reinterpret_cast<float *>(wb + WL.row);   // contiguous staged row
 
   const int64_t a0 = T.a_off[w];
@@ -670,7 +706,7 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
     // ---- partners
     PartnerSrc psrc{ax, ay, avis, A, i, px, py};
     float no_bound = 0.0f;
-    const int ma = select_topk<false>(psrc, cap_a, radius, D_fp64, S, lane, radius, no_bound);
+    const int ma = select_topk<true>(psrc, cap_a, radius, D_fp64, S, lane, radius, no_bound);
     float *ps = row + 7;
     for (int m = lane; m < ma; m += 32) {
       const int j = S.sel_pl[m];
@@ -719,7 +755,7 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
         const double rho = hint_radius(rho_hint, radius, D_fp64);
         RoadSrcGlobal rsrc{T.gpt_x, T.gpt_y, T.gpt_id, (int)p0, np, px, py, &geo};
         rsrc.cover(rho < radius ? rho : reach, lane);
-        mr = select_topk<true>(rsrc, cap_r, radius, D_fp64, S, lane, rho, bound);
+        mr = select_topk<false>(rsrc, cap_r, radius, D_fp64, S, lane, rho, bound);
       }
     }
     if (St.obs_hint && lane == 0)
