@@ -85,6 +85,25 @@ class RawWorlds:
             poly_pt_off=_offsets(counts_pts), pt_x=self.pt_x[p_idx], pt_y=self.pt_y[p_idx])
 
 
+def concat_raw(parts: list) -> "RawWorlds":
+    """Concatenate RawWorlds batches (world order preserved)."""
+    def cat(name):
+        return np.concatenate([getattr(p, name) for p in parts])
+
+    def off(name):
+        counts = np.concatenate([np.diff(getattr(p, name)) for p in parts])
+        return _offsets(counts)
+    return RawWorlds(
+        names=[n for p in parts for n in p.names], dt=cat("dt"), num_steps=cat("num_steps"),
+        a_off=off("a_off"), kind=cat("kind"), length=cat("length"), width=cat("width"),
+        goal=np.concatenate([p.goal.reshape(-1, 2) for p in parts]),
+        force_replay=cat("force_replay"), controllable=cat("controllable"), l_off=off("l_off"),
+        log_x=cat("log_x"), log_y=cat("log_y"), log_h=cat("log_h"), log_vx=cat("log_vx"),
+        log_vy=cat("log_vy"), log_valid=cat("log_valid"), poly_off=off("poly_off"),
+        poly_kind=cat("poly_kind"), poly_pt_off=off("poly_pt_off"), pt_x=cat("pt_x"),
+        pt_y=cat("pt_y"))
+
+
 def _offsets(counts) -> np.ndarray:
     out = np.zeros(len(counts) + 1, np.int64)
     if len(counts):

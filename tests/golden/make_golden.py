@@ -56,19 +56,26 @@ CONFIGS = {
                                     head=True),
 }
 FULL_OBS_STEPS = (0, 1, 91)
+# ragged batch (tests/ragged.py): hashes only, the GPU compares against the oracle
+RAGGED = {"ragged_nontrivial_radial": dict(dynamics="classic", collision_behavior="remove_agent",
+                                          init_mode="all_nontrivial", max_controlled_per_world=250,
+                                          obs=dict(mode="radial"))}
 
 
 def sha(a: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
 
 
-def make(name: str, spec: dict, n_worlds=3, n_agents=32, n_points=400, seed=21, steps=91):
-    raw = generate(WaymoSpec(n_worlds=n_worlds, n_agents=n_agents, n_points=n_points,
-                             seed=seed))
+def make(name: str, spec: dict, n_worlds=3, n_agents=32, n_points=400, seed=21, steps=91,
+         raw=None, full_obs=FULL_OBS_STEPS):
+    if raw is None:
+        raw = generate(WaymoSpec(n_worlds=n_worlds, n_agents=n_agents, n_points=n_points,
+                                 seed=seed))
     preps = to_scenarios(raw, rscn)
     obs = RObs(**spec["obs"])
     cfg = RCfg(dynamics=spec["dynamics"], collision_behavior=spec["collision_behavior"],
-               init_mode="all_valid", obs=obs)
+               init_mode=spec.get("init_mode", "all_valid"), obs=obs,
+               max_controlled_per_world=spec.get("max_controlled_per_world"))
     batch = RBatch(preps, cfg)
     n = batch.n_controlled
     rng = np.random.default_rng(zlib.crc32(name.encode()))
@@ -90,7 +97,8 @@ def make(name: str, spec: dict, n_worlds=3, n_agents=32, n_points=400, seed=21, 
         out[f"tab{w}_circumradius"] = world.circumradius
     acts, rews, dones, infos, hashes, poses = [], [], [], [], [], []
     hashes.append(sha(batch.observations))
-    out["obs_0"] = batch.observations.copy()
+    if 0 in full_obs:
+        out["obs_0"] = batch.observations.copy()
     head = spec.get("head", False)
     for t in range(1, steps + 1):
         a = np.column_stack([rng.uniform(-4, 4, n), rng.uniform(-0.7, 0.7, n)])
@@ -103,7 +111,7 @@ def make(name: str, spec: dict, n_worlds=3, n_agents=32, n_points=400, seed=21, 
         dones.append(o.dones.copy())
         infos.append(np.stack([o.info[k] for k in ("goal", "veh_collision", "offroad")]))
         hashes.append(sha(o.observations))
-        if t in FULL_OBS_STEPS:
+        if t in full_obs:
             out[f"obs_{t}"] = o.observations.copy()
         poses.append(np.concatenate([np.stack([w.pos[:, 0], w.pos[:, 1], w.heading, w.speed])
                                      for w in batch.worlds], 1))
@@ -131,6 +139,10 @@ def main():
                 "generator: paper_2408_01584_b200.synthetic (raw scene arrays stored in each npz)\n")
     for name, spec in CONFIGS.items():
         make(name, spec)
+    sys.path.insert(0, os.path.dirname(HERE))
+    from ragged import ragged_batch
+    for name, spec in RAGGED.items():
+        make(name, spec, raw=ragged_batch(seed=5), full_obs=())
 
 
 if __name__ == "__main__":

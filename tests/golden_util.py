@@ -27,7 +27,8 @@ def load(name: str):
                         "poly_pt_off", "pt_x", "pt_y")})
     spec = ast.literal_eval(str(z["cfg_json"]))
     cfg = SimConfig(dynamics=spec["dynamics"], collision_behavior=spec["collision_behavior"],
-                    init_mode="all_valid", obs=ObsConfig(**spec["obs"]))
+                    init_mode=spec.get("init_mode", "all_valid"), obs=ObsConfig(**spec["obs"]),
+                    max_controlled_per_world=spec.get("max_controlled_per_world"))
     return z, raw, cfg
 
 

@@ -47,25 +47,29 @@ def _gpu_out(batch):
             "dones": batch.dones.cpu().numpy(), "info": batch._info[:, :batch.n_controlled].cpu().numpy()}
 
 
-def run_free(case, steps=91, seed=0):
-    spec_kw, cfg_kw = CASES[case]
-    cfg = SimConfig(init_mode="all_valid", **cfg_kw)
-    raw = generate(WaymoSpec(seed=seed + 11, **spec_kw))
+def run_free(case, steps=91, seed=0, raw=None, cfg=None):
+    if raw is None:
+        spec_kw, cfg_kw = CASES[case]
+        cfg = SimConfig(init_mode="all_valid", **cfg_kw)
+        raw = generate(WaymoSpec(seed=seed + 11, **spec_kw))
+    lidar = cfg.obs.mode != "radial"
     batch = SimBatch.from_raw(raw, cfg, device="cuda:0")
     ora = OracleBatch(batch.packed, cfg)
     n = batch.n_controlled
     sel_w = cfg.obs.max_agents_obs + cfg.obs.max_road_points_obs
-    sel = torch.full((n, sel_w), -7, dtype=torch.int32, device="cuda:0")
+    sel = None if lidar else torch.full((n, sel_w), -7, dtype=torch.int32, device="cuda:0")
     batch.reset(sel_idx=sel)
+    sel_of = (lambda: None) if lidar else (lambda: sel.cpu().numpy())
+    ora_sel = (lambda: None) if lidar else (lambda: ora.sel_idx[:n])
     compare_step(0, _gpu_out(batch), (ora.observations, ora.rewards, ora.dones.astype(bool),
                                       {k: np.zeros(n, bool) for k in ("goal", "veh_collision", "offroad")}),
-                 sel.cpu().numpy(), ora.sel_idx[:n])
+                 sel_of(), ora_sel())
     rng = np.random.default_rng(seed)
     for t in range(1, steps + 1):
         act = actions_for(cfg, n, rng)
         batch.step(torch.from_numpy(act).cuda(), sel_idx=sel)
         o = ora.step(act.astype(np.float64))
-        compare_step(t, _gpu_out(batch), o, sel.cpu().numpy(), ora.sel_idx[:n])
+        compare_step(t, _gpu_out(batch), o, sel_of(), ora_sel())
     pw = batch.packed
     x, y, h = batch._x.cpu().numpy(), batch._y.cpu().numpy(), batch._h.cpu().numpy()
     nA = pw.n_agents
@@ -113,4 +117,35 @@ def test_auto_reset_env_semantics():
     eps = [(e.world_id, e.n_controlled, e.n_goal, e.n_veh_collision, e.n_offroad)
            for e in batch.episode_infos]
     assert eps == ora.episode_infos and len(eps) > 6
+    batch.close()
+
+
+@pytest.mark.parametrize("init_mode", ["all_nontrivial", "all_valid"])
+def test_ragged_batch_parity(init_mode):
+    """Worlds of 1..300 agents and 0..5000 road points, late entries, blink-outs,
+    never-valid and forced-replay agents, single-point road elements, agents
+    far off the map (tests/ragged.py)."""
+    from ragged import ragged_batch
+    cfg = SimConfig(init_mode=init_mode, collision_behavior="remove_agent",
+                    max_controlled_per_world=250)
+    run_free(None, raw=ragged_batch(seed=3), cfg=cfg)
+
+
+def test_ragged_batch_lidar_parity():
+    from ragged import ragged_batch
+    cfg = SimConfig(init_mode="all_valid", obs=ObsConfig(mode="lidar", n_rays=24, max_range=60.0))
+    run_free(None, raw=ragged_batch(seed=4, num_steps=30), cfg=cfg, steps=30)
+
+
+def test_view_cone_parity_with_head_rotation():
+    cfg = SimConfig(init_mode="all_valid", collision_behavior="remove_agent",
+                    obs=ObsConfig(mode="view_cone", n_rays=17, fov=2.5, max_range=70.0))
+    raw = generate(WaymoSpec(n_worlds=4, n_agents=40, n_points=1500, seed=8))
+    batch = SimBatch.from_raw(raw, cfg, device="cuda:0")
+    ora = OracleBatch(batch.packed, cfg)
+    rng = np.random.default_rng(2)
+    for t in range(1, 40):
+        act = actions_for(cfg, batch.n_controlled, rng, head=True)
+        batch.step(torch.from_numpy(act).cuda())
+        compare_step(t, _gpu_out(batch), ora.step(act.astype(np.float64)))
     batch.close()
