@@ -77,7 +77,7 @@ def _bin_segments(pw: PackedWorlds, sel: np.ndarray, world_of_seg: np.ndarray,
     kx = k % np.repeat(nxs, cnt)
     ky = k // np.repeat(nxs, cnt)
     cells = (cell_base[w[rep]] + (cy0[rep] + ky) * nx[w[rep]] + (cx0[rep] + kx)).astype(np.int64)
-    order = np.lexsort((idx[rep], cells))
+    order = np.argsort(cells, kind="stable")      # idx[rep] is already ascending
     cells_sorted = cells[order]
     counts = np.bincount(cells_sorted, minlength=n_cells_total)
     start = np.zeros(n_cells_total + 1, np.int64)
@@ -95,17 +95,12 @@ def build_layout(pw: PackedWorlds, cell: float = 8.0, all_segments: bool = True)
     x1 = np.zeros(W)
     y1 = np.zeros(W)
     has = P > 0
-    if len(world_of_pt):
-        mnx = np.full(W, big); mny = np.full(W, big)
-        mxx = np.full(W, -big); mxy = np.full(W, -big)
-        np.minimum.at(mnx, world_of_pt, pw.pt_x)
-        np.minimum.at(mny, world_of_pt, pw.pt_y)
-        np.maximum.at(mxx, world_of_pt, pw.pt_x)
-        np.maximum.at(mxy, world_of_pt, pw.pt_y)
-        x0 = np.where(has, mnx, 0.0)
-        y0 = np.where(has, mny, 0.0)
-        x1 = np.where(has, mxx, 0.0)
-        y1 = np.where(has, mxy, 0.0)
+    if has.any():
+        starts = pw.p_off[:-1][has]
+        x0[has] = np.minimum.reduceat(pw.pt_x, starts)
+        y0[has] = np.minimum.reduceat(pw.pt_y, starts)
+        x1[has] = np.maximum.reduceat(pw.pt_x, starts)
+        y1[has] = np.maximum.reduceat(pw.pt_y, starts)
     nx = (np.floor((x1 - x0) / cell).astype(np.int64) + 1)
     ny = (np.floor((y1 - y0) / cell).astype(np.int64) + 1)
     if (nx * ny > 1 << 26).any():
@@ -126,7 +121,7 @@ def build_layout(pw: PackedWorlds, cell: float = 8.0, all_segments: bool = True)
         gcell = cell_base[w] + cy * nx[w] + cx
     else:
         gcell = np.zeros(0, np.int64)
-    order = np.lexsort((local, gcell))       # world-major since cell ids are world-major
+    order = np.argsort(gcell, kind="stable")   # world-major cells, original order inside
     counts = np.bincount(gcell, minlength=n_cells_total)
     pstart = np.zeros(n_cells_total + 1, np.int64)
     np.cumsum(counts, out=pstart[1:])
@@ -158,8 +153,8 @@ def build_layout(pw: PackedWorlds, cell: float = 8.0, all_segments: bool = True)
     err = np.maximum(np.abs(gxy[:, 0].astype(np.float64) - relx),
                      np.abs(gxy[:, 1].astype(np.float64) - rely)) if len(ws) else np.zeros(0)
     eps = np.zeros(W)
-    if len(ws):
-        np.maximum.at(eps, ws, err)
+    if len(ws) and has.any():
+        eps[has] = np.maximum.reduceat(err, pw.p_off[:-1][has])
     return DeviceLayout(
         cell=float(cell), grid_x0=x0.astype(np.float64), grid_y0=y0.astype(np.float64),
         grid_nx=nx.astype(np.int32), grid_ny=ny.astype(np.int32), grid_cell_off=cell_base_ptr,

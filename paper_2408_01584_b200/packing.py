@@ -263,8 +263,10 @@ def pack(raw: RawWorlds, cfg: SimConfig) -> PackedWorlds:
     # First valid step per agent (engine.py:207-210).
     big = np.iinfo(np.int64).max
     first_valid = np.full(N, big, np.int64)
-    np.minimum.at(first_valid, np.repeat(np.arange(N), T_of_agent),
-                  np.where(raw.log_valid, loc_t, big))
+    nz = T_of_agent > 0
+    if nz.any():
+        first_valid[nz] = np.minimum.reduceat(np.where(raw.log_valid, loc_t, big),
+                                              agent_start[nz])
     instantiable = first_valid != big
     first_valid = np.where(instantiable, first_valid, T_of_agent)
     fv_cell = np.repeat(first_valid, T_of_agent)

@@ -57,11 +57,11 @@ def _quant(v):
     return np.round(np.asarray(v) / Q) * Q
 
 
-def _world(spec: WaymoSpec, wid: int):
+def _world_params(spec: WaymoSpec, wid: int):
+    """All random draws of one world, from its own stream (seed, world id)."""
     rng = np.random.default_rng([spec.seed, wid])
     L = spec.side
-    A, T, P = spec.n_agents, spec.num_steps, spec.n_points
-    # ---- agents
+    A, P = spec.n_agents, spec.n_points
     u = rng.random(A)
     kind = np.where(u < 0.8, 0, np.where(u < 0.9, 1, 2)).astype(np.int8)
     length = np.where(kind == 0, 4.6 + rng.uniform(-0.3, 0.3, A), np.where(kind == 1, 0.8, 1.8))
@@ -71,35 +71,22 @@ def _world(spec: WaymoSpec, wid: int):
     h = -rng.uniform(-math.pi, math.pi, A)          # (-pi, pi]
     v = rng.uniform(2.0, 15.0, A)
     steer = rng.uniform(-0.1, 0.1, A)
-    beta = np.arctan(0.5 * np.tan(steer))
-    lx = np.empty((A, T)); ly = np.empty((A, T)); lh = np.empty((A, T))
-    cx, cy, ch = x.copy(), y.copy(), h.copy()
-    for t in range(T):
-        lx[:, t], ly[:, t], lh[:, t] = _quant(cx), _quant(cy), ch
-        cx = cx + v * np.cos(ch + beta) * spec.dt
-        cy = cy + v * np.sin(ch + beta) * spec.dt
-        ch = np.mod(ch + v * np.cos(beta) * np.tan(steer) / length * spec.dt + math.pi,
-                    2 * math.pi) - math.pi
-        ch = np.where(ch <= -math.pi, ch + 2 * math.pi, ch)
-    vx = v[:, None] * np.cos(lh)
-    vy = v[:, None] * np.sin(lh)
-    goal = np.stack([lx[:, -1], ly[:, -1]], -1)
-    # ---- roads: polylines of 10..60 points summing to exactly P
-    lens = []
-    left = P
-    while left > 0:
-        n = int(rng.integers(10, 61))
-        if left - n < 10:
-            n = left
-        lens.append(n)
-        left -= n
-    lens = np.array(lens, np.int64)
+    # road polylines of 10..60 points summing to exactly P (a short tail is
+    # merged into the last polyline)
+    lens = rng.integers(10, 61, size=P // 10 + 2)
+    cum = np.cumsum(lens)
+    m = int(np.searchsorted(cum, P, side="left")) + 1
+    lens = lens[:m].copy()
+    lens[-1] -= int(cum[m - 1] - P)
+    if len(lens) > 1 and lens[-1] < 10:
+        lens[-2] += lens[-1]
+        lens = lens[:-1]
     R = len(lens)
     ku = rng.random(R)
-    cum = np.cumsum([KIND_P["road_edge"], KIND_P["lane"], KIND_P["road_line"]])
-    kinds = np.where(ku < cum[0], ROAD_KINDS.index("road_edge"),
-                     np.where(ku < cum[1], ROAD_KINDS.index("lane"),
-                              np.where(ku < cum[2], ROAD_KINDS.index("road_line"),
+    cuts = np.cumsum([KIND_P["road_edge"], KIND_P["lane"], KIND_P["road_line"]])
+    kinds = np.where(ku < cuts[0], ROAD_KINDS.index("road_edge"),
+                     np.where(ku < cuts[1], ROAD_KINDS.index("lane"),
+                              np.where(ku < cuts[2], ROAD_KINDS.index("road_line"),
                                        ROAD_KINDS.index("crosswalk")))).astype(np.int8)
     start = rng.uniform(0.0, L, (R, 2))
     h0 = rng.uniform(-math.pi, math.pi, R)
@@ -113,34 +100,49 @@ def _world(spec: WaymoSpec, wid: int):
     dy = 2.0 * np.sin(ang)
     dx[first] = 0.0
     dy[first] = 0.0
-    px = np.cumsum(dx); py = np.cumsum(dy)
+    px = np.cumsum(dx)
+    py = np.cumsum(dy)
     px = px - np.repeat(px[first], lens) + start[poly_of, 0]
     py = py - np.repeat(py[first], lens) + start[poly_of, 1]
-    return dict(kind=kind, length=length, width=width, goal=_quant(goal), lx=lx, ly=ly, lh=lh,
-                vx=vx, vy=vy, lens=lens, pkind=kinds, px=_quant(px), py=_quant(py))
+    return dict(kind=kind, length=length, width=width, x=x, y=y, h=h, v=v, steer=steer,
+                lens=lens, pkind=kinds, px=_quant(px), py=_quant(py))
 
 
 def generate(spec: WaymoSpec) -> RawWorlds:
     """RawWorlds for worlds [world_offset, world_offset + n_worlds)."""
-    parts = [_world(spec, spec.world_offset + k) for k in range(spec.n_worlds)]
+    parts = [_world_params(spec, spec.world_offset + k) for k in range(spec.n_worlds)]
     W, A, T = spec.n_worlds, spec.n_agents, spec.num_steps
     cat = lambda key: np.concatenate([p[key] for p in parts])
+    # classic-bicycle rollout with a = 0 and constant steer, all worlds at once
+    length, v, steer = cat("length"), cat("v"), cat("steer")
+    cx, cy, ch = cat("x").astype(np.float64), cat("y").astype(np.float64), cat("h")
+    beta = np.arctan(0.5 * np.tan(steer))
+    turn = v * np.cos(beta) * np.tan(steer) / length * spec.dt
+    N = W * A
+    lx = np.empty((N, T)); ly = np.empty((N, T)); lh = np.empty((N, T))
+    for t in range(T):
+        lx[:, t], ly[:, t], lh[:, t] = cx, cy, ch
+        cx = cx + v * np.cos(ch + beta) * spec.dt
+        cy = cy + v * np.sin(ch + beta) * spec.dt
+        ch = np.mod(ch + turn + math.pi, 2 * math.pi) - math.pi
+        ch = np.where(ch <= -math.pi, ch + 2 * math.pi, ch)
+    lx, ly = _quant(lx), _quant(ly)
+    vx = v[:, None] * np.cos(lh)
+    vy = v[:, None] * np.sin(lh)
+    goal = np.stack([lx[:, -1], ly[:, -1]], -1)
     lens = [p["lens"] for p in parts]
     raw = RawWorlds(
         names=[f"waymo-synth-{spec.seed}-{spec.world_offset + k}" for k in range(W)],
         dt=np.full(W, spec.dt), num_steps=np.full(W, T, np.int32),
-        a_off=_offsets([A] * W), kind=cat("kind"), length=cat("length"),
-        width=cat("width"), goal=cat("goal").reshape(-1, 2),
-        force_replay=np.zeros(W * A, bool), controllable=np.zeros(W * A, bool),
-        l_off=_offsets([A * T] * W), log_x=cat("lx").reshape(-1), log_y=cat("ly").reshape(-1),
-        log_h=cat("lh").reshape(-1), log_vx=cat("vx").reshape(-1), log_vy=cat("vy").reshape(-1),
-        log_valid=np.ones(W * A * T, bool),
-        poly_off=_offsets([len(l) for l in lens]), poly_kind=cat("pkind"),
-        poly_pt_off=_offsets(np.concatenate(lens)), pt_x=cat("px"), pt_y=cat("py"))
+        a_off=_offsets([A] * W), kind=cat("kind"), length=length, width=cat("width"),
+        goal=goal, force_replay=np.zeros(N, bool), controllable=np.zeros(N, bool),
+        l_off=_offsets([A * T] * W), log_x=lx.reshape(-1), log_y=ly.reshape(-1),
+        log_h=lh.reshape(-1), log_vx=vx.reshape(-1), log_vy=vy.reshape(-1),
+        log_valid=np.ones(N * T, bool), poly_off=_offsets([len(l) for l in lens]),
+        poly_kind=cat("pkind"), poly_pt_off=_offsets(np.concatenate(lens)), pt_x=cat("px"),
+        pt_y=cat("py"))
     # mark_controllable (scenario.py:371-384) with the default 2.0 m threshold
-    sx = raw.log_x.reshape(-1, T)[:, 0]
-    sy = raw.log_y.reshape(-1, T)[:, 0]
-    d = _native.host_hypot_cpython(sx - raw.goal[:, 0], sy - raw.goal[:, 1])
+    d = _native.host_hypot_cpython(lx[:, 0] - goal[:, 0], ly[:, 0] - goal[:, 1])
     raw.controllable = d > 2.0
     return raw
 
