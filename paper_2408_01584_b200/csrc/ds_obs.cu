@@ -36,28 +36,30 @@ constexpr int kCandShared = 224;  // (shared-points variant: hint-narrowed scans
 constexpr int kWarpsShared = 20;
 constexpr int kWarpsGlobal = 12;
 
-__host__ __device__ inline int kmax_of(const ds_config &c) {
-  int k = c.max_agents_obs > c.max_road_points_obs ? c.max_agents_obs : c.max_road_points_obs;
-  return k < 1 ? 1 : k;
+__host__ __device__ constexpr int kmax_of(int cap_a, int cap_r) {
+  return (cap_a > cap_r ? cap_a : cap_r) < 1 ? 1 : (cap_a > cap_r ? cap_a : cap_r);
 }
 
 // Capacity of the exactly ranked set G.
-__host__ __device__ inline int gcap_of(const ds_config &c) { return kmax_of(c) + 48; }
+__host__ __device__ constexpr int gcap_of(int cap_a, int cap_r) {
+  return kmax_of(cap_a, cap_r) + 48;
+}
 
-__host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
+__host__ __device__ constexpr size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
 
 // Per-warp shared scratch (byte offsets).  The observation row is staged
 // contiguously: [ego | partner slots] sit right before `hc`, and the road
 // block (11 floats per slot) aliases [hc ..), which is dead once the road
-// selection has produced sel_pl.
+// selection has produced sel_pl.  constexpr: with compile-time slot caps the
+// whole layout folds into immediate offsets off one base register.
 struct WarpLayout {
   size_t row, hc, ca, cp, ga, ge, gid, gpl, gb, gf, sel_pl, sel_id, total;
 };
 
-__host__ __device__ inline WarpLayout warp_layout(const ds_config &c, bool buffered) {
-  WarpLayout L;
-  const int km = kmax_of(c), gc = gcap_of(c);
-  const size_t head = (size_t)(7 + 7 * c.max_agents_obs) * sizeof(float);
+__host__ __device__ constexpr WarpLayout make_layout(int cap_a, int cap_r, bool buffered) {
+  WarpLayout L{};
+  const int km = kmax_of(cap_a, cap_r), gc = gcap_of(cap_a, cap_r);
+  const size_t head = (size_t)(7 + 7 * cap_a) * sizeof(float);
   size_t o = al16(head);
   L.row = o - head;
   L.hc = o; o = al16(o + kNB * sizeof(uint32_t));
@@ -70,12 +72,16 @@ __host__ __device__ inline WarpLayout warp_layout(const ds_config &c, bool buffe
   L.gpl = o; o = al16(o + gc * sizeof(int));
   L.gb = o; o = al16(o + gc);
   L.gf = o; o = al16(o + gc);
-  const size_t road_end = al16(L.hc + (size_t)c.max_road_points_obs * 11 * sizeof(float));
+  const size_t road_end = al16(L.hc + (size_t)cap_r * 11 * sizeof(float));
   if (o < road_end) o = road_end;
   L.sel_pl = o; o = al16(o + km * sizeof(int));
   L.sel_id = o; o = al16(o + km * sizeof(int));
   L.total = o;
   return L;
+}
+
+__host__ __device__ inline WarpLayout warp_layout(const ds_config &c, bool buffered) {
+  return make_layout(c.max_agents_obs, c.max_road_points_obs, buffered);
 }
 
 __host__ __device__ inline size_t agents_bytes(int max_agents) {
@@ -606,7 +612,9 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
 // ---------------------------------------------------------------------------
 // The kernel.  SharedPts: road points staged in shared memory (float2).
 // ---------------------------------------------------------------------------
-template <int WARPS, bool SharedPts>
+// CAPA / CAPR > 0: compile-time slot caps (the ObsConfig default 16 / 64);
+// 0: taken from the config at run time.
+template <int WARPS, bool SharedPts, int CAPA, int CAPR>
 __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kernel(
     ds_tables T, ds_config C, ds_state St, const uint8_t *mask, float *obs, const float *scale,
     int32_t *sel_idx, int obs_width) {
@@ -625,7 +633,10 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
   const int64_t p0 = T.p_off[w];
   const int np = (int)(T.p_off[w + 1] - p0);
   float2 *pts = reinterpret_cast<float2 *>(after_agents);
-  const WarpLayout WL = warp_layout(C, !SharedPts);
+  constexpr bool kFixed = CAPA > 0;
+  const int cap_a = kFixed ? CAPA : C.max_agents_obs, cap_r = kFixed ? CAPR : C.max_road_points_obs;
+  constexpr WarpLayout kWL = make_layout(CAPA, CAPR, !SharedPts);
+  const WarpLayout WL = kFixed ? kWL : warp_layout(C, !SharedPts);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char *wb = after_agents + (SharedPts ? al16((size_t)T.max_points * sizeof(float2)) : 0) +
                       WL.total * warp;
@@ -641,7 +652,7 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
   S.gf = wb + WL.gf;
   S.sel_pl = reinterpret_cast<int *>(wb + WL.sel_pl);
   S.sel_id = reinterpret_cast<int *>(wb + WL.sel_id);
-  S.gcap = gcap_of(C);
+  S.gcap = gcap_of(cap_a, cap_r);
   S.ccap = SharedPts ? kCandShared : kCandGlobal;
   float *row = reinterpret_cast<float *>(wb + WL.row);   // contiguous staged row
 
@@ -666,7 +677,6 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
 
   const double radius = C.radius;
   const double reach = radius + 1e-6;   // culling slack; membership is decided exactly
-  const int cap_a = C.max_agents_obs, cap_r = C.max_road_points_obs;
   const int road_off = 7 + 7 * cap_a;
   const int sel_w = cap_a + cap_r;
   const int nx = T.grid_nx[w], ny = T.grid_ny[w];
@@ -795,14 +805,16 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
 }
 
 cudaError_t configure_kernels(int max_dynamic_smem) {
-  cudaError_t e = cudaFuncSetAttribute(obs_radial_kernel<kWarpsShared, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       max_dynamic_smem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(obs_radial_kernel<kWarpsGlobal, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, max_dynamic_smem);
-  if (e != cudaSuccess) return e;
-  e = configure_lidar_kernels(max_dynamic_smem);
+  const void *ks[] = {(const void *)obs_radial_kernel<kWarpsShared, true, 16, 64>,
+                      (const void *)obs_radial_kernel<kWarpsShared, true, 0, 0>,
+                      (const void *)obs_radial_kernel<kWarpsGlobal, false, 16, 64>,
+                      (const void *)obs_radial_kernel<kWarpsGlobal, false, 0, 0>};
+  for (const void *k : ks) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         max_dynamic_smem);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = configure_lidar_kernels(max_dynamic_smem);
   if (e != cudaSuccess) return e;
   return configure_step_kernels(max_dynamic_smem);
 }
@@ -832,12 +844,22 @@ cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, float *obs,
     if (sel_idx) return cudaErrorInvalidValue;   // selection indices are radial-only
     return launch_lidar(h, mask, obs, scale, s);
   }
+  const bool fixed = h->cfg.max_agents_obs == 16 && h->cfg.max_road_points_obs == 64;
+  const int W = h->tab.n_worlds;
   if (h->obs_shared_pts) {
-    obs_radial_kernel<kWarpsShared, true><<<h->tab.n_worlds, kWarpsShared * 32, h->obs_smem, s>>>(
-        h->tab, h->cfg, h->st, mask, obs, scale, sel_idx, h->obs_width);
+    if (fixed)
+      obs_radial_kernel<kWarpsShared, true, 16, 64><<<W, kWarpsShared * 32, h->obs_smem, s>>>(
+          h->tab, h->cfg, h->st, mask, obs, scale, sel_idx, h->obs_width);
+    else
+      obs_radial_kernel<kWarpsShared, true, 0, 0><<<W, kWarpsShared * 32, h->obs_smem, s>>>(
+          h->tab, h->cfg, h->st, mask, obs, scale, sel_idx, h->obs_width);
   } else {
-    obs_radial_kernel<kWarpsGlobal, false><<<h->tab.n_worlds, kWarpsGlobal * 32, h->obs_smem, s>>>(
-        h->tab, h->cfg, h->st, mask, obs, scale, sel_idx, h->obs_width);
+    if (fixed)
+      obs_radial_kernel<kWarpsGlobal, false, 16, 64><<<W, kWarpsGlobal * 32, h->obs_smem, s>>>(
+          h->tab, h->cfg, h->st, mask, obs, scale, sel_idx, h->obs_width);
+    else
+      obs_radial_kernel<kWarpsGlobal, false, 0, 0><<<W, kWarpsGlobal * 32, h->obs_smem, s>>>(
+          h->tab, h->cfg, h->st, mask, obs, scale, sel_idx, h->obs_width);
   }
   return cudaGetLastError();
 }
