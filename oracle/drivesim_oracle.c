@@ -19,8 +19,9 @@
  *   radial_fill_core      _fastpath.py:214-302 (linear scan + insertion top-k)
  *   fill_lidar            observation.py:223-280 with raycast_obbs_arr
  *                         geometry.py:399-424 and raycast_segments_arr 380-396
- *                         (segment candidates in index order instead of BVH
- *                         order: differs only on exact distance ties).
+ *                         (an exact distance tie between a road edge and another
+ *                         kind goes to the edge; the reference breaks it in BVH
+ *                         order).
  *   delta_local dynamics  (not in the reference; DESIGN.md definition)
  *
  * Compiled with -O2 -ffp-contract=off (no FMA contraction, like numba's
@@ -320,7 +321,10 @@ static void lidar_row(const or_tables *T, const or_config *C, const or_state *S,
       double t = (wx * ey - wy * ex) / denom;
       double u = (wx * dy - wy * dx) / denom;
       if (!(t >= 0.0 && u >= 0.0 && u <= 1.0)) continue;
-      if (t < smin) { smin = t; sedge = T->seg_kind[q] == ROAD_EDGE; }
+      /* nearest wins; an exact tie between a road edge and another kind goes
+       * to the edge (the reference breaks such ties in BVH order) */
+      const int is_edge = T->seg_kind[q] == ROAD_EDGE;
+      if (t < smin || (t == smin && is_edge && !sedge)) { smin = t; sedge = is_edge; }
     }
     if (smin < best) { best = smin; best_type = sedge ? 1 : 2; }
     if (best > max_range) { best = max_range; best_type = 3; }

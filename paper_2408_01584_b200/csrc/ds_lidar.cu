@@ -9,16 +9,21 @@
 //    passes farther than its circumradius (+1 mm) from its centre or it lies
 //    behind the origin -- a superset test -- then the exact FP64 slab test
 //    of raycast_obbs_arr gives the distance; the minimum is the agent hit;
-//  * road segments: the ray walks the world's uniform grid row band by row
-//    band in increasing distance, testing the segments binned in the covered
-//    cells with the exact FP64 formula of raycast_segments_arr; the walk
-//    stops once the next band starts beyond the best hit.  The first minimal
-//    segment in index order wins (the reference takes the first in BVH
-//    order; the two differ only for exact distance ties between segments of
-//    different kinds);
+//  * road segments, segment-major: the warp visits the grid cells of the
+//    max-range disc ring by ring around the origin's cell, skips cells whose
+//    rays all hit something nearer already, and strides its lanes over the
+//    segments binned in the surviving cells (flattened, full warp batches);
+//    each segment is tested with the exact FP64 formula of
+//    raycast_segments_arr only against the rays inside its angular span seen
+//    from the origin, and merged per ray with one 64-bit atomicMin on
+//    (distance bits << 1 | not_edge): nearest wins, an exact-distance tie
+//    between a road edge and another road kind resolves to the edge (the
+//    reference resolves such ties in its BVH traversal order, the oracle
+//    uses the same edge-first rule);
 //  * a road replaces the box hit only if strictly nearer; beyond max_range
 //    the ray reports max_range with type none.
 #include "ds_internal.cuh"
+#include "ds_rows.cuh"
 
 namespace ds {
 
@@ -33,14 +38,66 @@ __host__ __device__ inline size_t lidar_agents_bytes(int amax) {
   return al16l((size_t)amax * (7 * sizeof(double) + 1));
 }
 
+// per warp: ray dx, dy, box-min bits, segment-key min, limit (8 B each) + row
 __host__ __device__ inline size_t lidar_warp_bytes(int obs_width, int n_rays) {
-  return al16l((size_t)n_rays * 3 * sizeof(double) + (size_t)obs_width * sizeof(float));
+  return al16l((size_t)n_rays * 5 * sizeof(double) + (size_t)obs_width * sizeof(float));
 }
 
-__device__ __forceinline__ int clampl(double f, int lo, int hi) {
-  if (f < (double)lo) return lo;
-  if (f > (double)hi) return hi;
-  return (int)f;
+constexpr double kInvTwoPi = 0.15915494309189535;
+
+// atan2 for |(x, y)| > 0 with |error| < 3e-6 rad (octant reduction + odd
+// minimax polynomial); only used for conservative angular ray ranges
+__device__ __forceinline__ float fast_atan2(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float a = __fdividef(fminf(ax, ay), fmaxf(ax, ay));
+  const float s = a * a;
+  float r = a * (0.99997726f + s * (-0.33262347f + s * (0.19354346f + s * (-0.11643287f +
+                s * (0.05265332f + s * -0.01172120f)))));
+  if (ay > ax) r = 1.57079637f - r;
+  if (x < 0.0f) r = 3.14159274f - r;
+  return y < 0.0f ? -r : r;
+}
+
+// Ray indices whose direction can lie in the angular interval [rel, rel +
+// span] (rel in [0, 2pi) relative to the sweep centre, already widened):
+// full circle rays at 2 pi k / R (range may run past R - 1, callers wrap),
+// cone rays at -fov/2 + fov k / (R - 1) (interval tried at rel and rel - 2pi).
+__device__ __forceinline__ void ray_range(float rel, float span, bool full, int R, double fov,
+                                          int &k_lo, int &k_hi) {
+  if (full) {
+    const float scl = (float)R * (float)kInvTwoPi;
+    k_lo = (int)floorf(rel * scl);
+    k_hi = (int)ceilf((rel + span) * scl);
+    if (k_hi - k_lo + 1 >= R) {
+      k_lo = 0;
+      k_hi = R - 1;
+    }
+    return;
+  }
+  if (R == 1) {
+    k_lo = 0;
+    k_hi = 0;
+    return;
+  }
+  const float scl = (float)(R - 1) / (float)fov, hf = 0.5f * (float)fov;
+  int lo = R, hi = -1;
+  for (int sh = 0; sh < 2; ++sh) {
+    const float rr = sh == 0 ? rel : rel - (float)kTwoPi;
+    const int a2 = max((int)floorf((rr + hf) * scl), 0);
+    const int b2 = min((int)ceilf((rr + span + hf) * scl), R - 1);
+    if (a2 <= b2) {
+      lo = min(lo, a2);
+      hi = max(hi, b2);
+    }
+  }
+  k_lo = lo;
+  k_hi = hi;
+}
+
+// current upper bound of ray k's road search: the box hit / max_range limit
+// or the best segment so far (an unset key decodes to NaN, ignored by fmin)
+__device__ __forceinline__ double ray_bound(double lim, unsigned long long seg_key) {
+  return fmin(lim, __longlong_as_double((long long)(seg_key >> 1)));
 }
 
 // raycast_segments_arr (geo:380-396) for one ray and one segment, returning
@@ -97,81 +154,6 @@ __device__ __forceinline__ double ray_box(double ox, double oy, double dx, doubl
   return ok ? fmax(tmin, 0.0) : INFINITY;
 }
 
-struct SegGrid {
-  const int *cell_start;   // world's all-segment cell CSR (absolute)
-  const double *ax, *ay, *bx, *by;
-  const int *sid;
-  const uint8_t *edge;
-  double gx0, gy0, cs, inv_cs;
-  int nx, ny;
-};
-
-// Nearest segment hit along (ox, oy) + t (dx, dy), t <= limit; returns
-// (t, edge) of the first minimal segment in index order.
-__device__ double walk_segments(const SegGrid &G, double ox, double oy, double dx, double dy,
-                                double limit, bool &edge_out) {
-  double best = INFINITY;
-  int best_id = 0x7fffffff;
-  bool best_edge = false;
-  if (G.nx <= 0 || G.ny <= 0) {
-    edge_out = false;
-    return best;
-  }
-  const double slack = 1e-6;
-  const double y_end = oy + dy * limit;
-  const int iya = clampl(floor((oy - G.gy0) * G.inv_cs), -1, G.ny);
-  const int iyb = clampl(floor((y_end - G.gy0) * G.inv_cs), -1, G.ny);
-  const int step = iyb >= iya ? 1 : -1;
-  const double inv_dy = dy != 0.0 ? 1.0 / dy : 0.0;
-  for (int iy = iya;; iy += step) {
-    if (iy >= 0 && iy < G.ny) {
-      const double ylo = G.gy0 + iy * G.cs - slack, yhi = G.gy0 + (iy + 1) * G.cs + slack;
-      double t0, t1;
-      if (dy == 0.0) {
-        if (oy < ylo || oy > yhi) {
-          t0 = 1.0;
-          t1 = 0.0;
-        } else {
-          t0 = 0.0;
-          t1 = limit;
-        }
-      } else {
-        const double ta = (ylo - oy) * inv_dy, tb = (yhi - oy) * inv_dy;
-        t0 = fmax(0.0, fmin(ta, tb) - 1e-9);
-        t1 = fmin(limit, fmax(ta, tb) + 1e-9);
-      }
-      if (t0 > best) break;   // bands further out only hold larger distances
-      if (t0 <= t1) {
-        const double xa = ox + dx * t0, xb = ox + dx * t1;
-        const double xl = fmin(xa, xb) - slack, xh = fmax(xa, xb) + slack;
-        if (!(xh < G.gx0 || xl > G.gx0 + G.nx * G.cs)) {
-          const int ix0 = clampl(floor((xl - G.gx0) * G.inv_cs), 0, G.nx - 1);
-          const int ix1 = clampl(floor((xh - G.gx0) * G.inv_cs), 0, G.nx - 1);
-          const int *c = G.cell_start + (int64_t)iy * G.nx;
-          const int b = c[ix0], e = c[ix1 + 1];
-          for (int k = b; k < e; ++k) {
-            const double beat = best < limit ? best : limit;
-            const double t =
-                ray_segment(ox, oy, dx, dy, G.ax[k], G.ay[k], G.bx[k], G.by[k], beat);
-            if (t < best || (t == best && G.sid[k] < best_id)) {
-              if (t != INFINITY) {
-                best = t;
-                best_id = G.sid[k];
-                best_edge = G.edge[k];
-              }
-            }
-          }
-        }
-      }
-    } else if ((step > 0 && iy >= G.ny) || (step < 0 && iy < 0)) {
-      break;
-    }
-    if (iy == iyb) break;
-  }
-  edge_out = best_edge;
-  return best;
-}
-
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
     ds_tables T, ds_config C, ds_state St, const uint8_t *mask, float *obs, const float *scale,
@@ -192,8 +174,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
   unsigned char *wb = smem_raw + lidar_agents_bytes(amax) + (size_t)warp * per_warp;
   double *rdx = reinterpret_cast<double *>(wb);
   double *rdy = rdx + C.n_rays;
-  unsigned long long *rbest = reinterpret_cast<unsigned long long *>(rdy + C.n_rays);
-  float *row = reinterpret_cast<float *>(rbest + C.n_rays);
+  double *rlim = rdy + C.n_rays;
+  unsigned long long *rbest = reinterpret_cast<unsigned long long *>(rlim + C.n_rays);
+  unsigned long long *rseg = rbest + C.n_rays;
+  float *row = reinterpret_cast<float *>(rseg + C.n_rays);
 
   const int64_t a0 = T.a_off[w];
   const int A = (int)(T.a_off[w + 1] - a0);
@@ -211,18 +195,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
   }
   __syncthreads();
 
-  SegGrid G;
   const int64_t cbase = T.grid_cell_off[w];
-  G.cell_start = T.aseg_cell_start + cbase;
-  G.ax = T.aseg_ax; G.ay = T.aseg_ay; G.bx = T.aseg_bx; G.by = T.aseg_by;
-  G.sid = T.aseg_id;
-  G.edge = T.aseg_edge;
-  G.gx0 = T.grid_x0[w];
-  G.gy0 = T.grid_y0[w];
-  G.cs = C.grid_cell;
-  G.inv_cs = 1.0 / C.grid_cell;
-  G.nx = T.grid_nx[w];
-  G.ny = T.grid_ny[w];
+  const double gx0 = T.grid_x0[w], gy0 = T.grid_y0[w], cs = C.grid_cell;
+  const int gnx = T.grid_nx[w], gny = T.grid_ny[w];
   const double max_range = C.max_range;
   const int R = C.n_rays;
   const bool full_circle = C.obs_mode == DS_OBS_LIDAR || C.fov >= kTwoPi;
@@ -315,16 +290,121 @@ __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
       }
     }
     __syncwarp();
+    // per-ray limit for the segment phase: the box hit or max_range
     for (int k = lane; k < R; k += 32) {
-      const double dx = rdx[k], dy = rdy[k];
+      rlim[k] = fmin(__longlong_as_double((long long)rbest[k]), max_range) * (1.0 + 1e-12) + 1e-9;
+      rseg[k] = 0xffffffffffffffffull;
+    }
+    __syncwarp();
+    // road segments, segment-major, grid cells in Chebyshev rings around the
+    // origin's cell (nearest first); a cell of ring >= 2 is skipped when every
+    // ray of its angular span already has a hit nearer than the cell, and the
+    // walk stops once no ray can still be improved by the remaining rings
+    {
+      const double inv_cs = 1.0 / cs;
+      const int ocx = (int)fmin(fmax(floor((ox - gx0) * inv_cs), -1e6), 1e6);
+      const int ocy = (int)fmin(fmax(floor((oy - gy0) * inv_cs), -1e6), 1e6);
+      const double reach = max_range + 1e-6;
+      const int rmax = (int)ceil(reach * inv_cs) + 1;
+      const float fcenter = (float)center;
+      const float cell_rad = (float)(cs * 0.7071067811865476) + 1e-3f;
+      for (int ring = 0; ring <= rmax; ++ring) {
+        const int ncell = ring == 0 ? 1 : 8 * ring;
+        for (int q0 = 0; q0 < ncell; q0 += 32) {
+          const int q = q0 + lane;
+          int sb = 0, cnt = 0;
+          if (q < ncell) {
+            int ix = ocx, iy = ocy;
+            if (ring > 0) {
+              const int side = q / (2 * ring), pos = q - side * 2 * ring;
+              if (side == 0) { ix = ocx - ring + pos; iy = ocy - ring; }
+              else if (side == 1) { ix = ocx + ring; iy = ocy - ring + pos; }
+              else if (side == 2) { ix = ocx + ring - pos; iy = ocy + ring; }
+              else { ix = ocx - ring; iy = ocy + ring - pos; }
+            }
+            if (ix >= 0 && ix < gnx && iy >= 0 && iy < gny) {
+              const double xlo = gx0 + ix * cs, ylo = gy0 + iy * cs;
+              const double ddx = fmax(fmax(xlo - ox, ox - (xlo + cs)), 0.0);
+              const double ddy = fmax(fmax(ylo - oy, oy - (ylo + cs)), 0.0);
+              const double dmin = sqrt(ddx * ddx + ddy * ddy);
+              bool keep = dmin <= reach;
+              if (keep && ring >= 2) {
+                // bounding-circle angular span of the cell (ring >= 2: the
+                // origin is at least 1.5 cells from the cell centre)
+                const float ccx = (float)(xlo + 0.5 * cs - ox), ccy = (float)(ylo + 0.5 * cs - oy);
+                const float dc = sqrtf(ccx * ccx + ccy * ccy);
+                const float half = asinf(fminf(1.0f, cell_rad / dc)) + 1e-4f;
+                float rel = fast_atan2(ccy, ccx) - half - fcenter;
+                rel -= (float)kTwoPi * floorf(rel * (float)kInvTwoPi);
+                int k_lo, k_hi;
+                ray_range(rel, 2.0f * half, full_circle, R, C.fov, k_lo, k_hi);
+                const double need = dmin - 1e-6;
+                keep = false;
+                for (int m = k_lo; m <= k_hi && !keep; ++m) {
+                  const int k = m >= R ? m - R : m;
+                  keep = !(ray_bound(rlim[k], rseg[k]) < need);
+                }
+              }
+              if (keep) {
+                const int *c = T.aseg_cell_start + cbase + (int64_t)iy * gnx + ix;
+                sb = c[0];
+                cnt = c[1] - sb;
+              }
+            }
+          }
+          FlatRows cells;
+          cells.build(sb, cnt, lane);
+          for (int f0 = 0; f0 < cells.total; f0 += 32) {
+            const int e = cells.map(f0, lane);
+            if (f0 + lane >= cells.total) continue;
+            const double ax = T.aseg_ax[e], ay = T.aseg_ay[e], bx = T.aseg_bx[e], by = T.aseg_by[e];
+            const unsigned long long not_edge = T.aseg_edge[e] ? 0ull : 1ull;
+            // angular span of the segment seen from the origin (float, widened)
+            const float fax = (float)(ax - ox), fay = (float)(ay - oy);
+            const float fbx = (float)(bx - ox), fby = (float)(by - oy);
+            int k_lo = 0, k_hi = R - 1;
+            if (fminf(fax * fax + fay * fay, fbx * fbx + fby * fby) > 1.0f) {
+              const float pa = fast_atan2(fay, fax), pb = fast_atan2(fby, fbx);
+              float dlt = pb - pa;
+              if (dlt > (float)kPi) dlt -= (float)kTwoPi;
+              if (dlt < -(float)kPi) dlt += (float)kTwoPi;
+              if (fabsf(dlt) < (float)kPi - 1e-3f) {
+                float rel = (dlt >= 0.0f ? pa : pb) - 1e-4f - fcenter;
+                rel -= (float)kTwoPi * floorf(rel * (float)kInvTwoPi);   // [0, 2pi)
+                ray_range(rel, fabsf(dlt) + 2e-4f, full_circle, R, C.fov, k_lo, k_hi);
+              }
+            }
+            for (int m = k_lo; m <= k_hi; ++m) {
+              const int k = m >= R ? m - R : m;
+              const double lim = rlim[k];
+              const double beat = ray_bound(lim, rseg[k]);
+              const double t = ray_segment(ox, oy, rdx[k], rdy[k], ax, ay, bx, by, beat);
+              if (t <= lim)
+                atomicMin(&rseg[k], ((unsigned long long)__double_as_longlong(t + 0.0) << 1) | not_edge);
+            }
+          }
+        }
+        __syncwarp();
+        // rings beyond `ring` lie at least ring * cs from the origin
+        if (ring >= 1) {
+          const double far = ring * cs - 1e-6;
+          bool open = false;
+          for (int k = lane; k < R; k += 32) open = open || !(ray_bound(rlim[k], rseg[k]) < far);
+          if (!__any_sync(kFullMask, open)) break;
+        }
+      }
+    }
+    __syncwarp();
+    for (int k = lane; k < R; k += 32) {
       double best = __longlong_as_double((long long)rbest[k]);
       int type = best != INFINITY ? 0 : 3;
-      bool edge = false;
-      const double limit = fmin(best, max_range) * (1.0 + 1e-12) + 1e-9;
-      const double smin = walk_segments(G, ox, oy, dx, dy, limit, edge);
-      if (smin < best) {
-        best = smin;
-        type = edge ? 1 : 2;
+      const unsigned long long sk = rseg[k];
+      if (sk != 0xffffffffffffffffull) {
+        const double smin = __longlong_as_double((long long)(sk >> 1));
+        if (smin < best) {
+          best = smin;
+          type = (sk & 1ull) ? 2 : 1;
+        }
       }
       if (best > max_range) {
         best = max_range;

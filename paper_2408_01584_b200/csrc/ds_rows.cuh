@@ -1,0 +1,92 @@
+// ds_rows.cuh -- cell-row ranges of a query disc over a world's uniform
+// grid (device_layout.py), flattened into full 32-wide warp batches.
+#pragma once
+
+#include "ds_internal.cuh"
+
+namespace ds {
+
+constexpr unsigned kFullMask = 0xffffffffu;
+
+__device__ __forceinline__ int clampi(double f, int lo, int hi) {
+  if (f < (double)lo) return lo;
+  if (f > (double)hi) return hi;
+  return (int)f;
+}
+
+// Cell rows of a query disc around (px, py): lane l owns row iy0 + l; the
+// covered cells of a row are one contiguous range of the cell-sorted points.
+struct RowGeo {
+  const int *cell_start;   // world's cell CSR (absolute point indices)
+  double px, py, gx0, gy0, cs, inv_cs;
+  int nx, ny, iy0, nrows;
+  __device__ __forceinline__ void init(double reach) {
+    const double fy0 = (py - reach - gy0) * inv_cs, fy1 = (py + reach - gy0) * inv_cs;
+    iy0 = 0;
+    nrows = 0;
+    if (nx > 0 && ny > 0 && fy1 >= 0.0 && fy0 < (double)ny) {
+      iy0 = clampi(floor(fy0), 0, ny - 1);
+      nrows = clampi(floor(fy1), 0, ny - 1) - iy0 + 1;
+      nrows = nrows < 32 ? nrows : 32;
+    }
+  }
+  // range of lane's row for radius `reach` (a superset of the disc's points)
+  __device__ __forceinline__ void range(double reach, int lane, int &sb, int &cnt) const {
+    sb = 0;
+    cnt = 0;
+    if (lane >= nrows) return;
+    const int iy = iy0 + lane;
+    const double ylo = gy0 + iy * cs, yhi = ylo + cs;
+    double dyb = 0.0;
+    if (py < ylo) dyb = ylo - py;
+    else if (py > yhi) dyb = py - yhi;
+    if (dyb > reach) return;
+    const double half = sqrt(reach * reach - dyb * dyb) + 1e-6;
+    const double fx0 = (px - half - gx0) * inv_cs, fx1 = (px + half - gx0) * inv_cs;
+    if (fx1 < 0.0 || fx0 >= (double)nx) return;
+    const int ix0 = clampi(floor(fx0), 0, nx - 1), ix1 = clampi(floor(fx1), 0, nx - 1);
+    const int *c = cell_start + (int64_t)iy * nx;
+    sb = c[ix0];
+    cnt = c[ix1 + 1] - sb;
+  }
+};
+
+// Non-empty cell rows compacted to lanes 0..n-1 with inclusive prefix ends,
+// so candidates are visited in full 32-wide batches across row boundaries.
+// Lane o of the batch starting at f0 maps to row #(ends <= f0) plus the
+// number of row ends inside (f0, f0 + o]: one OR-reduction of end offsets
+// and a popcount (ends are distinct because empty rows were dropped).
+struct FlatRows {
+  int sb, cnt, pe, nr, total;
+  __device__ __forceinline__ void build(int sb_in, int cnt_in, int lane) {
+    const unsigned bal = __ballot_sync(kFullMask, cnt_in > 0);
+    nr = __popc(bal);
+    int src = (int)__fns(bal, 0, lane + 1);
+    src = (src >= 0 && src < 32) ? src : 0;
+    sb = __shfl_sync(kFullMask, sb_in, src);
+    cnt = __shfl_sync(kFullMask, cnt_in, src);
+    if (lane >= nr) cnt = 0;
+    pe = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int up = __shfl_up_sync(kFullMask, pe, off);
+      if (lane >= off) pe += up;
+    }
+    total = __shfl_sync(kFullMask, pe, 31);
+  }
+  // point index of flattened candidate f0 + lane (valid when f0 + lane < total)
+  __device__ __forceinline__ int map(int f0, int lane) const {
+    const bool live = lane < nr;
+    const int r0 = __popc(__ballot_sync(kFullMask, live && pe <= f0));
+    const int off = pe - f0;
+    const unsigned E = __reduce_or_sync(kFullMask, (live && off > 0 && off < 32) ? (1u << off) : 0u);
+    const int r = (r0 + __popc(E & ((2u << lane) - 1u))) & 31;
+    const int rs = __shfl_sync(kFullMask, sb, r);
+    const int rpe = __shfl_sync(kFullMask, pe, r);
+    const int rc = __shfl_sync(kFullMask, cnt, r);
+    return rs + (f0 + lane - (rpe - rc));
+  }
+};
+
+
+}  // namespace ds
