@@ -155,7 +155,7 @@ __device__ __forceinline__ double ray_box(double ox, double oy, double dx, doubl
 }
 
 template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
+__global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
     ds_tables T, ds_config C, ds_state St, const uint8_t *mask, float *obs, const float *scale,
     int obs_width) {
   const int w = blockIdx.x;
@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
     const int i = (int)(g - a0);
     const uint16_t f = St.flags[g];
     if (f & (DS_F_DONE | DS_F_REMOVED)) {
+      #pragma unroll 1
       for (int c = lane; c < obs_width; c += 32) out[c] = 0.0f;
       continue;
     }
@@ -227,14 +228,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
     }
     double center = h;
     if (C.obs_mode == DS_OBS_VIEW_CONE) center += St.head_angle[g];
+    const float fcenter = (float)center;
     // ray directions (_ray_angles, obs:213-220) and per-ray box minima
+    #pragma unroll 1
     for (int k = lane; k < R; k += 32) {
       double ang;
       if (full_circle) ang = center + (2.0 * kPi * (double)k) / (double)R;
       else if (R == 1) ang = center;
       else ang = (center - 0.5 * C.fov) + (C.fov * (double)k) / (double)(R - 1);
-      rdx[k] = cos(ang);
-      rdy[k] = sin(ang);
+      sincos(ang, &rdy[k], &rdx[k]);
       rbest[k] = 0x7ff0000000000000ull;   // +inf
     }
     __syncwarp();
@@ -243,47 +245,22 @@ __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
     // of a conservative angular interval around its bounding circle
     for (int j = lane; j < A; j += 32) {
       if (j == i || !svis[j]) continue;
-      const double cx = sx[j] - ox, cy = sy[j] - oy;
-      const double cr = scr[j];
-      if (!(hypot(cx, cy) <= max_range + cr)) continue;
-      const double dist = sqrt(cx * cx + cy * cy);
+      // float superset of the candidates: a box whose centre is farther
+      // than max_range + circumradius cannot be hit within max_range
+      const float cx = (float)(sx[j] - ox), cy = (float)(sy[j] - oy);
+      const float cr = (float)scr[j] + 1e-3f;
+      const float d2 = cx * cx + cy * cy, lim = (float)max_range + cr + 1e-3f;
+      if (d2 > lim * lim) continue;
       int k_lo = 0, k_hi = R - 1;
-      bool all = dist <= cr + 1e-3;
-      double rel = 0.0, half = 0.0;
-      if (!all) {
-        half = asin(fmin(1.0, (cr + 1e-3) / dist)) + 1e-6;
-        rel = atan2(cy, cx) - center;
-        rel -= kTwoPi * floor(rel / kTwoPi);           // [0, 2pi)
-      }
-      if (full_circle && !all) {
-        const double scl = (double)R / kTwoPi;
-        k_lo = (int)floor((rel - half) * scl - 1e-6);
-        k_hi = (int)ceil((rel + half) * scl + 1e-6);
-        if (k_hi - k_lo + 1 >= R) {
-          k_lo = 0;
-          k_hi = R - 1;
-        }
-      }
-      if (!full_circle && !all && R > 1) {
-        // cone rays sit at rel angles -fov/2 + fov k/(R-1); try the interval
-        // around rel and around rel - 2pi (cone centred on 0)
-        const double scl = (double)(R - 1) / C.fov;
-        int lo = R, hi = -1;
-        for (int sh = 0; sh < 2; ++sh) {
-          const double rr = sh == 0 ? rel : rel - kTwoPi;
-          const int a = (int)floor((rr - half + 0.5 * C.fov) * scl - 1e-6);
-          const int b = (int)ceil((rr + half + 0.5 * C.fov) * scl + 1e-6);
-          const int a2 = a < 0 ? 0 : a, b2 = b > R - 1 ? R - 1 : b;
-          if (a2 <= b2) {
-            lo = min(lo, a2);
-            hi = max(hi, b2);
-          }
-        }
-        k_lo = lo;
-        k_hi = hi;
+      const float dist = sqrtf(d2);
+      if (dist > cr + 1e-3f) {
+        const float half = asinf(fminf(1.0f, cr / dist)) + 1e-4f;
+        float rel = fast_atan2(cy, cx) - half - fcenter;
+        rel -= (float)kTwoPi * floorf(rel * (float)kInvTwoPi);   // [0, 2pi)
+        ray_range(rel, 2.0f * half, full_circle, R, C.fov, k_lo, k_hi);
       }
       for (int m = k_lo; m <= k_hi; ++m) {
-        const int k = ((m % R) + R) % R;
+        const int k = m >= R ? m - R : m;
         const double d = ray_box(ox, oy, rdx[k], rdy[k], sx[j], sy[j], sc[j], ss[j], shl[j], shw[j]);
         if (d != INFINITY)   // d >= 0; + 0.0 maps -0 to +0 so the bit order is the value order
           atomicMin(&rbest[k], (unsigned long long)__double_as_longlong(d + 0.0));
@@ -291,6 +268,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
     }
     __syncwarp();
     // per-ray limit for the segment phase: the box hit or max_range
+    #pragma unroll 1
     for (int k = lane; k < R; k += 32) {
       rlim[k] = fmin(__longlong_as_double((long long)rbest[k]), max_range) * (1.0 + 1e-12) + 1e-9;
       rseg[k] = 0xffffffffffffffffull;
@@ -306,7 +284,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
       const int ocy = (int)fmin(fmax(floor((oy - gy0) * inv_cs), -1e6), 1e6);
       const double reach = max_range + 1e-6;
       const int rmax = (int)ceil(reach * inv_cs) + 1;
-      const float fcenter = (float)center;
       const float cell_rad = (float)(cs * 0.7071067811865476) + 1e-3f;
       for (int ring = 0; ring <= rmax; ++ring) {
         const int ncell = ring == 0 ? 1 : 8 * ring;
@@ -389,12 +366,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
         if (ring >= 1) {
           const double far = ring * cs - 1e-6;
           bool open = false;
+          #pragma unroll 1
           for (int k = lane; k < R; k += 32) open = open || !(ray_bound(rlim[k], rseg[k]) < far);
           if (!__any_sync(kFullMask, open)) break;
         }
       }
     }
     __syncwarp();
+    #pragma unroll 1
     for (int k = lane; k < R; k += 32) {
       double best = __longlong_as_double((long long)rbest[k]);
       int type = best != INFINITY ? 0 : 3;
@@ -419,8 +398,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) obs_lidar_kernel(
     }
     __syncwarp();
     if (scale) {
+      #pragma unroll 1
       for (int c = lane; c < obs_width; c += 32) out[c] = row[c] / scale[c];
     } else {
+      #pragma unroll 1
       for (int c = lane; c < obs_width; c += 32) out[c] = row[c];
     }
     __syncwarp();
