@@ -9,8 +9,10 @@
 
 #ifdef __CUDACC__
 #define DS_HD __host__ __device__ __forceinline__
+#define DS_HD_COLD static __host__ __device__ __noinline__
 #else
 #define DS_HD static inline
+#define DS_HD_COLD static
 #endif
 
 namespace ds {
@@ -66,7 +68,10 @@ DS_HD double hypot_kernel(double ax, double ay) {
   return h;
 }
 
-DS_HD double hypot(double x, double y) {
+// scaled / non-finite / degenerate cases of hypot() below (out of line: they
+// are cold, and keeping one inline copy of the common path keeps the
+// observation kernels' code small)
+DS_HD_COLD double hypot_slow(double x, double y) {
   const double kScale = 0x1p-600, kLarge = 0x1p+511, kTiny = 0x1p-511, kEps = 0x1p-54;
   if (!isfinite(x) || !isfinite(y)) {
     if ((isinf(x) || isinf(y)) && !isnan(x) && !isnan(y)) return INFINITY;
@@ -88,6 +93,16 @@ DS_HD double hypot(double x, double y) {
   }
   if (ay <= ax * kEps) return ax + ay;
   return hypot_kernel(ax, ay);
+}
+
+DS_HD double hypot(double x, double y) {
+  // common case (finite, unscaled, non-degenerate): glibc's branch order
+  // reaches hypot_kernel(ax, ay) directly; NaN fails every comparison
+  const double kLarge = 0x1p+511, kTiny = 0x1p-511, kEps = 0x1p-54;
+  const double fx = fabs(x), fy = fabs(y);
+  const double ax = fx < fy ? fy : fx, ay = fx < fy ? fx : fy;
+  if (ax <= kLarge && ay >= kTiny && ay > ax * kEps) return hypot_kernel(ax, ay);
+  return hypot_slow(x, y);
 }
 
 DS_HD double clip(double v, double lo, double hi) {

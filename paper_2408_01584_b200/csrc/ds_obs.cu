@@ -136,6 +136,7 @@ struct PartnerSrc {
   __device__ __forceinline__ bool small_payload() const { return true; }
   template <class F>
   __device__ __forceinline__ void visit(float r2hi, int lane, F &&fn) const {
+    #pragma unroll 1
     for (int f0 = 0; f0 < n; f0 += 32) {
       const int f = f0 + lane;
       bool ok = f < n && f != self && vis[f];
@@ -177,6 +178,7 @@ struct RoadSrcShared {
   __device__ __forceinline__ bool small_payload() const { return true; }
   template <class F>
   __device__ __forceinline__ void visit(float r2hi, int lane, F &&fn) const {
+    #pragma unroll 1
     for (int f0 = 0; f0 < rows.total; f0 += 32) {
       const int s = rows.map(f0, lane);
       bool ok = f0 + lane < rows.total;
@@ -214,6 +216,7 @@ struct RoadSrcGlobal {
   __device__ __forceinline__ bool small_payload() const { return np <= 0xffff; }
   template <class F>
   __device__ __forceinline__ void visit(float r2hi, int lane, F &&fn) const {
+    #pragma unroll 1
     for (int f0 = 0; f0 < rows.total; f0 += 32) {
       const int s = rows.map(f0, lane);
       bool ok = f0 + lane < rows.total;
@@ -615,8 +618,10 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
     const uint16_t f = St.flags[g];
     if (f & (DS_F_DONE | DS_F_REMOVED)) {
       // finished / removed rows are zero-filled (engine.py:502-512)
+      #pragma unroll 1
       for (int c = lane; c < obs_width; c += 32) out[c] = 0.0f;
       if (sel_idx)
+        #pragma unroll 1
         for (int c = lane; c < sel_w; c += 32) sel_idx[orow * sel_w + c] = -1;
       continue;
     }
@@ -717,8 +722,10 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
     __syncwarp();
     // ---- coalesced write-out of the staged row
     if (scale) {
+      #pragma unroll 1
       for (int c = lane; c < obs_width; c += 32) out[c] = row[c] / scale[c];
     } else {
+      #pragma unroll 1
       for (int c = lane; c < obs_width; c += 32) out[c] = row[c];
     }
     __syncwarp();
