@@ -42,6 +42,7 @@ CONFIGS = {
            "VecDriveEnv + in-loop ActorCritic policy"),
 }
 # CPU sample of the same workload for the oracle legs: worlds stepped per "step"
+L2_BYTES = 126 * 1024 * 1024   # B200 L2
 CPU_WORLDS = {"c1": 16, "c2": 128, "c3": 64, "c4": 8, "c5": 64}
 
 
@@ -216,18 +217,33 @@ class CpuSample:
             act = self.rng.uniform([-4, -0.7], [4, 0.7], (n, 2))
         self.ora.step(act.astype(np.float32).astype(np.float64), auto_reset=True)
 
-    def rate(self, steps: int, warmup: int = 1, budget_s: float = 30.0):
+    def rate(self, steps: int, warmup: int = 1, budget_s: float = 30.0, min_s: float = 0.0):
+        """At least `steps` steps (and at least min_s seconds of them), at
+        most budget_s seconds."""
         for _ in range(warmup):
             self.step()
         t0 = time.perf_counter()
         k = 0
-        while k < steps:
+        while k < steps or time.perf_counter() - t0 < min_s:
             self.step()
             k += 1
             if time.perf_counter() - t0 > budget_s:
                 break
         el = time.perf_counter() - t0
         return self.agents * k / el, f"{self.desc} x {k} steps ({el:.1f} s)"
+
+
+def bench_config(name: str, W: int, W_total: int, world: int,
+                 l2: str = "working set > L2 (no flush needed)") -> dict:
+    """The `config` object of a bench line (both arms print the same one)."""
+    from paper_2408_01584_b200.config import obs_width
+    _, A, P, dyn, coll, okw, workload = CONFIGS[name]
+    cfg = sim_config(name)
+    return {"workload": workload, "worlds_per_gpu": W, "worlds_total": W_total,
+            "agents": A, "road_points": P, "dynamics": dyn, "collision": coll,
+            "obs_mode": cfg.obs.mode, "obs_width": obs_width(cfg.obs), "episode_steps": 91,
+            "auto_reset": True, "l2": l2,
+            "parallelism": f"world shards x {world} GPU (no step collective)"}
 
 
 def run_reference(args, rank):
@@ -238,13 +254,17 @@ def run_reference(args, rank):
     threads = os.cpu_count() or 1
     cs = CpuSample(args.config, threads)
     value, sample = cs.rate(args.steps, warmup=args.warmup, budget_s=120.0)
-    W, A, P, dyn, coll, okw, workload = CONFIGS[args.config]
+    W = args.worlds or CONFIGS[args.config][0]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    W_total = W if args.strong else W * world
+    if args.strong:
+        W = -(-W // world)
     line = {"impl": "reference", "metric": "agent_steps_per_sec", "value": value,
             "unit": "agent-steps/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload, "worlds_per_gpu": W, "agents": A, "road_points": P,
-                       "dynamics": dyn, "collision": coll, "obs": okw or {"mode": "radial"}},
+            "config": bench_config(args.config, W, W_total, world),
             "cpu_baseline": {"value": value, "unit": "agent-steps/s", "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "agent-steps/s", "h2d_bytes_per_step": 0,
@@ -261,6 +281,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--worlds", type=int, default=None, help="override worlds per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: the config's worlds split over the ranks "
+                         "(default weak: the config's worlds on every rank)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -276,17 +299,32 @@ def main():
     from paper_2408_01584_b200.engine import SimBatch, random_actions
     from paper_2408_01584_b200.synthetic import WaymoSpec, generate
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # DS_BENCH_SHARE_GPU=1 (test only): ranks share the visible GPUs over gloo,
+    # to exercise the N > 1 path on a one-GPU box; never used for bench lines
+    share = os.environ.get("DS_BENCH_SHARE_GPU") == "1"
+    gpu = local_rank % torch.cuda.device_count() if share else local_rank
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     W, A, P, dyn, coll, okw, workload = CONFIGS[args.config]
     if args.worlds:
         W = args.worlds
+    W_total = W * world
+    w_off = rank * W
+    if args.strong:
+        import numpy as np
+        from paper_2408_01584_b200.parallel import shard_ranges
+        W_total = W
+        lo, hi = shard_ranges(np.ones(W), world)[rank]
+        W, w_off = hi - lo, lo
     cfg = sim_config(args.config)
     width = obs_width(cfg.obs)
     t_setup = time.perf_counter()
-    raw = generate(WaymoSpec(n_worlds=W, n_agents=A, n_points=P, seed=0, world_offset=rank * W))
+    raw = generate(WaymoSpec(n_worlds=W, n_agents=A, n_points=P, seed=0, world_offset=w_off))
     rl = args.config == "c5"
     if rl:
         from paper_2408_01584_b200.env import EnvConfig, VecDriveEnv
@@ -331,6 +369,16 @@ def main():
             e.record(stream)
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
+    # small working sets (C1, C2 at a few worlds) would stay L2-resident across
+    # steps: flush L2 (write 2x its size) before every timed step and time the
+    # steps individually instead
+    ws = torch.cuda.memory_allocated(dev)
+    flush_l2 = ws < L2_BYTES * 2
+    l2_note = (f"L2 flushed before each timed step (working set {ws / 1e6:.0f} MB)" if flush_l2
+               else f"working set {ws / 1e6:.0f} MB > 2x L2 (no flush needed)")
+    flush_buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if flush_l2 else None
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
     torch.cuda.synchronize(dev)
     sampler = ClockSampler(local_rank)
     sampler.start()
@@ -339,12 +387,19 @@ def main():
     torch.cuda.synchronize(dev)
     start.record(stream)
     for t in range(args.steps):
+        if flush_l2:
+            flush_buf.fill_(float(t))
+            step_ev[t][0].record(stream)
         one_step(t, events=ev[t])
+        if flush_l2:
+            step_ev[t][1].record(stream)
     end.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
     clocks = sampler.stop()
     ms = start.elapsed_time(end)
+    if flush_l2:
+        ms = sum(a.elapsed_time(b) for a, b in step_ev)
     kernel_ms = None
     if not rl:
         kernel_ms = {"step_kernel": sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps,
@@ -353,7 +408,12 @@ def main():
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    agents_total = batch.total_agents * world
+    # units all ranks processed: every rank's agents (allreduce of the counts)
+    agents_total = batch.total_agents
+    if world > 1:
+        ta = torch.tensor([float(agents_total)], device=dev)
+        dist.all_reduce(ta)
+        agents_total = int(ta.item())
     value = agents_total * args.steps / (ms / 1e3)
 
     # ---- end to end through the public API with host buffers: every step
@@ -421,7 +481,8 @@ def main():
         if not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
             try:
-                v, sample = CpuSample(args.config, threads).rate(91, warmup=1, budget_s=10.0)
+                v, sample = CpuSample(args.config, threads).rate(91, warmup=1, budget_s=20.0,
+                                                                  min_s=10.0)
                 cpu = {"value": v, "unit": "agent-steps/s", "cores": threads, "kind": "port",
                        "sample": sample}
             except Exception as exc:   # report, never fake
@@ -431,13 +492,10 @@ def main():
         result = {
             "metric": "agent_steps_per_sec", "value": value, "unit": "agent-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload, "worlds_per_gpu": W, "agents": A, "road_points": P,
-                       "dynamics": dyn, "collision": coll, "obs_mode": cfg.obs.mode,
-                       "obs_width": width, "episode_steps": 91, "auto_reset": True,
-                       "l2": "working set > L2 (no flush needed)",
-                       "parallelism": f"world shards x {world} GPU (no step collective)"},
+            "config": bench_config(args.config, W, W_total, world, l2_note),
             "e2e": {"value": e2e_value, "unit": "agent-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": (2 * args.steps) if not rl else 2 * args.steps,
