@@ -34,7 +34,7 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNB = 256;       // histogram buckets
 constexpr int kCandGlobal = 640;  // buffered pass-1 candidates (global-points variant)
 constexpr int kCandShared = 224;  // (shared-points variant: hint-narrowed scans)
-constexpr int kWarpsShared = 20;
+constexpr int kWarpsShared = 24;
 constexpr int kWarpsGlobal = 12;
 
 __host__ __device__ constexpr int kmax_of(int cap_a, int cap_r) {
@@ -60,15 +60,22 @@ struct WarpLayout {
 __host__ __device__ constexpr WarpLayout make_layout(int cap_a, int cap_r, bool buffered) {
   WarpLayout L{};
   const int km = kmax_of(cap_a, cap_r), gc = gcap_of(cap_a, cap_r);
+  // the staged row may sit up to 3 floats before `row` (it is shifted so
+  // that its 16-B phase matches the output row's, for float4 write-out)
   const size_t head = (size_t)(7 + 7 * cap_a) * sizeof(float);
-  size_t o = al16(head);
+  size_t o = al16(head) + 16;
   L.row = o - head;
   L.hc = o; o = al16(o + kNB * sizeof(uint32_t));
   const int cc = buffered ? kCandGlobal : kCandShared;
-  L.ca = o; o = al16(o + cc * sizeof(float));
-  L.cp = o; o = al16(o + cc * sizeof(uint16_t));
+  // the buffered pass-1 candidates (ca, cp) are dead once pass 2 has
+  // scattered them into G; the exact distances ge of G alias them
+  L.ca = o;
+  L.ge = o;
+  const size_t cand_end = al16(al16(o + cc * sizeof(float)) + cc * sizeof(uint16_t));
+  L.cp = al16(o + cc * sizeof(float));
+  const size_t ge_end = al16(o + gc * sizeof(double));
+  o = cand_end > ge_end ? cand_end : ge_end;
   L.ga = o; o = al16(o + gc * sizeof(float));
-  L.ge = o; o = al16(o + gc * sizeof(double));
   L.gid = o; o = al16(o + gc * sizeof(int));
   L.gpl = o; o = al16(o + gc * sizeof(int));
   L.gb = o; o = al16(o + gc);
@@ -85,8 +92,9 @@ __host__ __device__ inline WarpLayout warp_layout(const ds_config &c, bool buffe
   return make_layout(c.max_agents_obs, c.max_road_points_obs, buffered);
 }
 
+// per agent: x, y, heading, speed, length, width, cos, sin (f64) + visible (u8)
 __host__ __device__ inline size_t agents_bytes(int max_agents) {
-  return al16((size_t)max_agents * (6 * sizeof(double) + 1));
+  return al16((size_t)max_agents * (8 * sizeof(double) + 1));
 }
 
 size_t obs_smem_bytes_shared(const ds_config &cfg, int max_agents, int max_points) {
@@ -551,8 +559,8 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
   const int amax = T.max_agents;
   double *ax = reinterpret_cast<double *>(smem_raw);
   double *ay = ax + amax, *ah = ax + 2 * amax, *av = ax + 3 * amax, *al = ax + 4 * amax,
-         *aw = ax + 5 * amax;
-  uint8_t *avis = reinterpret_cast<uint8_t *>(ax + 6 * amax);
+         *aw = ax + 5 * amax, *ac = ax + 6 * amax, *as = ax + 7 * amax;
+  uint8_t *avis = reinterpret_cast<uint8_t *>(ax + 8 * amax);
   unsigned char *after_agents = smem_raw + agents_bytes(amax);
   const int64_t p0 = T.p_off[w];
   const int np = (int)(T.p_off[w + 1] - p0);
@@ -578,7 +586,8 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
   S.sel_id = reinterpret_cast<int *>(wb + WL.sel_id);
   S.gcap = gcap_of(cap_a, cap_r);
   S.ccap = SharedPts ? kCandShared : kCandGlobal;
-  float *row = reinterpret_cast<float *>(wb + WL.row);   // contiguous staged row
+  float *const row0 = reinterpret_cast<float *>(wb + WL.row);
+  const int row0_phase = (int)((reinterpret_cast<uintptr_t>(row0) >> 2) & 3);
 
   const int64_t a0 = T.a_off[w];
   const int A = (int)(T.a_off[w + 1] - a0);
@@ -587,6 +596,8 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
     ax[i] = St.x[g];
     ay[i] = St.y[g];
     ah[i] = St.heading[g];
+    ac[i] = cos(ah[i]);
+    as[i] = sin(ah[i]);
     av[i] = St.speed[g];
     al[i] = T.length[g];
     aw[i] = T.width[g];
@@ -616,17 +627,26 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
     const int64_t g = T.row_agent[orow];
     const int i = (int)(g - a0);
     const uint16_t f = St.flags[g];
+    // 16-B phase of the output row; the staged row copies it
+    const int out_phase = (int)((reinterpret_cast<uintptr_t>(out) >> 2) & 3);
+    const int head = (4 - out_phase) & 3;           // floats until out is 16-B aligned
+    const int nvec = obs_width > head ? (obs_width - head) >> 2 : 0;
     if (f & (DS_F_DONE | DS_F_REMOVED)) {
       // finished / removed rows are zero-filled (engine.py:502-512)
+      if (lane < head && lane < obs_width) out[lane] = 0.0f;
       #pragma unroll 1
-      for (int c = lane; c < obs_width; c += 32) out[c] = 0.0f;
+      for (int v = lane; v < nvec; v += 32)
+        reinterpret_cast<float4 *>(out + head)[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      #pragma unroll 1
+      for (int c = head + 4 * nvec + lane; c < obs_width; c += 32) out[c] = 0.0f;
       if (sel_idx)
         #pragma unroll 1
         for (int c = lane; c < sel_w; c += 32) sel_idx[orow * sel_w + c] = -1;
       continue;
     }
+    float *const row = row0 - ((row0_phase - out_phase) & 3);   // contiguous staged row
     const double px = ax[i], py = ay[i], h = ah[i];
-    const double ch = cos(h), sh = sin(h);
+    const double ch = ac[i], sh = as[i];
     if (lane == 0) {
       // ego block (fp:228-238)
       const double gx = T.goal_x[g] - px, gy = T.goal_y[g] - py;
@@ -720,13 +740,31 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
       }
     }
     __syncwarp();
-    // ---- coalesced write-out of the staged row
-    if (scale) {
-      #pragma unroll 1
-      for (int c = lane; c < obs_width; c += 32) out[c] = row[c] / scale[c];
-    } else {
-      #pragma unroll 1
-      for (int c = lane; c < obs_width; c += 32) out[c] = row[c];
+    // ---- coalesced write-out of the staged row: scalar head, float4 body
+    // (the staged row has the output's 16-B phase), scalar tail
+    {
+      const float4 *rv = reinterpret_cast<const float4 *>(row + head);
+      float4 *ov = reinterpret_cast<float4 *>(out + head);
+      const int tail0 = head + 4 * nvec;
+      if (scale) {
+        if (lane < head && lane < obs_width) out[lane] = row[lane] / scale[lane];
+        #pragma unroll 1
+        for (int v = lane; v < nvec; v += 32) {
+          float4 x = rv[v];
+          const float *sc = scale + head + 4 * v;
+          x.x /= sc[0];
+          x.y /= sc[1];
+          x.z /= sc[2];
+          x.w /= sc[3];
+          ov[v] = x;
+        }
+        for (int c = tail0 + lane; c < obs_width; c += 32) out[c] = row[c] / scale[c];
+      } else {
+        if (lane < head && lane < obs_width) out[lane] = row[lane];
+        #pragma unroll 1
+        for (int v = lane; v < nvec; v += 32) ov[v] = rv[v];
+        for (int c = tail0 + lane; c < obs_width; c += 32) out[c] = row[c];
+      }
     }
     __syncwarp();
   }
