@@ -438,6 +438,38 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     });
     bound_out = 0.0f;
     if (n == 0) return 0;
+    __syncwarp();
+    if (n <= 32) {
+      // one candidate per lane: warp bitonic sort by (key, payload); keys more
+      // than 2D apart order exactly like the distances, so the sorted order is
+      // the reference's unless a near tie or a possibly-out-of-radius key sits
+      // inside the first k (then the exact ranking below decides)
+      float a = lane < n ? S.ga[lane] : INFINITY;
+      int pl = lane < n ? S.gpl[lane] : 0x7fffffff;
+#pragma unroll
+      for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          const float oa = __shfl_xor_sync(kFull, a, stride);
+          const int opl = __shfl_xor_sync(kFull, pl, stride);
+          const bool o_less = oa < a || (oa == a && opl < pl);
+          const bool want_min = ((lane & stride) == 0) == ((lane & size) == 0 || size == 32);
+          if (want_min == o_less) {
+            a = oa;
+            pl = opl;
+          }
+        }
+      }
+      const float an = __shfl_down_sync(kFull, a, 1);
+      const bool bad = lane < k && lane < n &&
+                       ((lane + 1 < n && an <= a + two_d) || (double)a > r2 - D);
+      if (!__any_sync(kFull, bad)) {
+        const int m = n < k ? n : k;
+        if (lane < m) S.sel_pl[lane] = pl;
+        __syncwarp();
+        return m;
+      }
+    }
     if (n <= S.gcap && n <= 0xffff) {
       if (lane == 0) S.hc[0] = ((uint32_t)n << 16) | (uint32_t)n;
       __syncwarp();
