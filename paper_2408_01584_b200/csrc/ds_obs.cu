@@ -314,12 +314,15 @@ __device__ __forceinline__ double sel_r2hi(double radius, double D) {
 }
 
 // Radius that provably contains the k nearest candidates given a hint that
-// bounds the k-th distance (triangle inequality), widened so that the
-// selection's bucket window (b* + 2) stays inside it.
+// bounds the k-th distance (triangle inequality).  The narrowed selection
+// histograms [0, rho^2] (bucket width w = rho^2 / kNB); the k-th key is
+// <= hint^2 + D, so the bucket window b* + 2 (+1.01 slack) stays inside
+// rho^2 - D when rho^2 (1 - 3.05 / kNB) >= hint^2 + 2D.  The floor
+// rho^2 >= 10240 D keeps the edge band beta = 2 D kNB / rho^2 <= 0.05.
 __device__ __forceinline__ double hint_radius(double hint, double radius, double D) {
   if (!(hint > 0.0)) return radius;
-  const double w = sel_r2hi(radius, D) / kNB;
-  return fmin(sqrt(hint * hint + 3.1 * w + D) + 1e-3, radius);
+  const double r2n = fmax((hint * hint + 2.0 * D) / (1.0 - 3.05 / kNB) + 1e-3, 10240.0 * D);
+  return fmin(sqrt(r2n), radius);
 }
 
 // Rank the set G[0, n_g) (bucket-sorted, counting-sort cursors in S.hc) with
@@ -416,14 +419,21 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
                            double rho, float &bound_out) {
   if (k <= 0) return 0;
   const double r2 = radius * radius;
-  const float r2hi = (float)((r2 + D) * (1.0 + 1e-7) + 1e-30);
-  const float inv_w = r2hi > 0.0f ? (float)kNB / r2hi : 0.0f;
-  const double w = (double)r2hi / kNB;
-  // edge band in bucket units: twice the key error plus float slack
-  const float beta = (float)(2.0 * D * (double)inv_w) + 4e-5f;
+  // histogram range [0, r2hi] in key units: the whole disc, or [0, rho^2]
+  // for a hint-narrowed scan (finer buckets, see hint_radius)
+  float r2hi, inv_w, beta, two_d;
+  double w;
+  auto set_range = [&](double top) {
+    r2hi = (float)(top * (1.0 + 1e-7) + 1e-30);
+    inv_w = r2hi > 0.0f ? (float)kNB / r2hi : 0.0f;
+    w = (double)r2hi / kNB;
+    // edge band in bucket units: twice the key error plus float slack
+    beta = (float)(2.0 * D * (double)inv_w) + 4e-5f;
+    // near-tie band in float, padded by the float rounding of a - 2D
+    two_d = (float)(2.0 * D + 2.5e-7 * (double)r2hi);
+  };
+  set_range(r2 + D);
   if (!(beta < 0.125f)) return select_serial(src, k, radius, r2hi, S, lane);
-  // near-tie band in float, padded by the float rounding of a - 2D
-  const float two_d = (float)(2.0 * D + 2.5e-7 * (double)r2hi);
   if (Direct) {
     int n = 0;
     src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
@@ -479,6 +489,7 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     __syncwarp();
   }
   bool restricted = rho < radius;
+  if (restricted) set_range(rho * rho);
   const int pb = src.pbase();
   const bool small = src.small_payload();
   constexpr int kPer = kNB / 32;
@@ -527,6 +538,7 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     if (restricted && !((((double)bmax + 1.01) * w + D) <= rho * rho)) {
       src.restrict_to(radius + 1e-6, lane);
       restricted = false;
+      set_range(r2 + D);
       continue;
     }
     break;
