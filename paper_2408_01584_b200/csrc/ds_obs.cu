@@ -590,32 +590,41 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
 // ---------------------------------------------------------------------------
 // CAPA / CAPR > 0: compile-time slot caps (the ObsConfig default 16 / 64);
 // 0: taken from the config at run time.
+// Per-launch scalars derived from the config on the host: kernel parameters
+// live in the constant bank, so the kernel uses them as operands instead of
+// keeping (or rematerialising) them in registers.
+struct RadialK {
+  double radius, reach, r2, D_fp64, cs, inv_cs, key_e;
+};
+
 template <int WARPS, bool SharedPts, int CAPA, int CAPR>
 __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kernel(
-    ds_tables T, ds_config C, ds_state St, const uint8_t *mask, float *obs, const float *scale,
-    int32_t *sel_idx, int obs_width) {
+    ds_tables T, ds_config C, ds_state St, const RadialK K, const uint8_t *mask, float *obs,
+    const float *scale, int32_t *sel_idx, int obs_width) {
   const int w = blockIdx.x;
   if (mask && !mask[w]) return;
   const int64_t c0 = T.c_off[w];
   const int nrow = (int)(T.c_off[w + 1] - c0);
   if (nrow == 0) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int amax = T.max_agents;
-  double *ax = reinterpret_cast<double *>(smem_raw);
-  double *ay = ax + amax, *ah = ax + 2 * amax, *av = ax + 3 * amax, *al = ax + 4 * amax,
-         *aw = ax + 5 * amax, *ac = ax + 6 * amax, *as = ax + 7 * amax;
-  uint8_t *avis = reinterpret_cast<uint8_t *>(ax + 8 * amax);
-  unsigned char *after_agents = smem_raw + agents_bytes(amax);
-  const int64_t p0 = T.p_off[w];
-  const int np = (int)(T.p_off[w + 1] - p0);
-  float2 *pts = reinterpret_cast<float2 *>(after_agents);
   constexpr bool kFixed = CAPA > 0;
   const int cap_a = kFixed ? CAPA : C.max_agents_obs, cap_r = kFixed ? CAPR : C.max_road_points_obs;
   constexpr WarpLayout kWL = make_layout(CAPA, CAPR, !SharedPts);
   const WarpLayout WL = kFixed ? kWL : warp_layout(C, !SharedPts);
+  // shared memory: [per-warp scratch x WARPS][road points][agents] -- the
+  // scratch and the points sit at (compile-time) constant offsets
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char *wb = after_agents + (SharedPts ? al16((size_t)T.max_points * sizeof(float2)) : 0) +
-                      WL.total * warp;
+  unsigned char *wb = smem_raw + WL.total * warp;
+  unsigned char *after_scratch = smem_raw + WL.total * WARPS;
+  float2 *pts = reinterpret_cast<float2 *>(after_scratch);
+  const int amax = T.max_agents;
+  double *ax = reinterpret_cast<double *>(
+      after_scratch + (SharedPts ? al16((size_t)T.max_points * sizeof(float2)) : 0));
+  double *ay = ax + amax, *ah = ax + 2 * amax, *av = ax + 3 * amax, *al = ax + 4 * amax,
+         *aw = ax + 5 * amax, *ac = ax + 6 * amax, *as = ax + 7 * amax;
+  uint8_t *avis = reinterpret_cast<uint8_t *>(ax + 8 * amax);
+  const int64_t p0 = T.p_off[w];
+  const int np = (int)(T.p_off[w + 1] - p0);
   Sel S;
   S.hc = reinterpret_cast<uint32_t *>(wb + WL.hc);
   S.ca = reinterpret_cast<float *>(wb + WL.ca);
@@ -654,16 +663,16 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
   }
   __syncthreads();
 
-  const double radius = C.radius;
-  const double reach = radius + 1e-6;   // culling slack; membership is decided exactly
+  const double radius = K.radius;
+  const double reach = K.reach;         // culling slack; membership is decided exactly
   const int road_off = 7 + 7 * cap_a;
   const int sel_w = cap_a + cap_r;
   const int nx = T.grid_nx[w], ny = T.grid_ny[w];
-  const double gx0 = T.grid_x0[w], gy0 = T.grid_y0[w], cs = C.grid_cell;
-  const double inv_cs = 1.0 / cs;
+  const double gx0 = T.grid_x0[w], gy0 = T.grid_y0[w], cs = K.cs;
+  const double inv_cs = K.inv_cs;
   const int64_t cbase = T.grid_cell_off[w];
   const double eps_p = SharedPts ? T.grid_eps[w] : 0.0;
-  const double D_fp64 = (radius * radius + 1.0) * 2.4e-7;   // fl32 of an FP64 d^2
+  const double D_fp64 = K.D_fp64;       // fl32 of an FP64 d^2
 
   for (int r = warp; r < nrow; r += WARPS) {
     const int64_t orow = c0 + r;
@@ -744,8 +753,7 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
         const double rx = px - gx0, ry = py - gy0;
         const float prx = (float)rx, pry = (float)ry;
         // key bound: |dx_f - dx| <= E; |a - d^2| <= 4 (r + 1) E + 2 E^2 + fl32 rounding
-        const double E = eps_p + fmax(fabs((double)prx - rx), fabs((double)pry - ry)) +
-                         (radius + 1.0) * 1.2e-7;
+        const double E = eps_p + fmax(fabs((double)prx - rx), fabs((double)pry - ry)) + K.key_e;
         const double D = 4.0 * (radius + 1.0) * E + 2.0 * E * E + D_fp64;
         const double rho = hint_radius(rho_hint, radius, D);
         RoadSrcShared rsrc{pts, T.gpt_x, T.gpt_y, T.gpt_id, (int)p0, prx, pry, px, py, &geo};
@@ -856,20 +864,28 @@ cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, float *obs,
   }
   const bool fixed = h->cfg.max_agents_obs == 16 && h->cfg.max_road_points_obs == 64;
   const int W = h->tab.n_worlds;
+  RadialK K;
+  K.radius = h->cfg.radius;
+  K.reach = K.radius + 1e-6;
+  K.r2 = K.radius * K.radius;
+  K.D_fp64 = (K.radius * K.radius + 1.0) * 2.4e-7;
+  K.cs = h->cfg.grid_cell;
+  K.inv_cs = 1.0 / K.cs;
+  K.key_e = (K.radius + 1.0) * 1.2e-7;
   if (h->obs_shared_pts) {
     if (fixed)
       obs_radial_kernel<kWarpsShared, true, 16, 64><<<W, kWarpsShared * 32, h->obs_smem, s>>>(
-          h->tab, h->cfg, h->st, mask, obs, scale, sel_idx, h->obs_width);
+          h->tab, h->cfg, h->st, K, mask, obs, scale, sel_idx, h->obs_width);
     else
       obs_radial_kernel<kWarpsShared, true, 0, 0><<<W, kWarpsShared * 32, h->obs_smem, s>>>(
-          h->tab, h->cfg, h->st, mask, obs, scale, sel_idx, h->obs_width);
+          h->tab, h->cfg, h->st, K, mask, obs, scale, sel_idx, h->obs_width);
   } else {
     if (fixed)
       obs_radial_kernel<kWarpsGlobal, false, 16, 64><<<W, kWarpsGlobal * 32, h->obs_smem, s>>>(
-          h->tab, h->cfg, h->st, mask, obs, scale, sel_idx, h->obs_width);
+          h->tab, h->cfg, h->st, K, mask, obs, scale, sel_idx, h->obs_width);
     else
       obs_radial_kernel<kWarpsGlobal, false, 0, 0><<<W, kWarpsGlobal * 32, h->obs_smem, s>>>(
-          h->tab, h->cfg, h->st, mask, obs, scale, sel_idx, h->obs_width);
+          h->tab, h->cfg, h->st, K, mask, obs, scale, sel_idx, h->obs_width);
   }
   return cudaGetLastError();
 }
