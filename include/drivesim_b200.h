@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define DS_ABI_VERSION 1
+#define DS_ABI_VERSION 2
 #define DS_MAX_AGENTS_PER_WORLD 1024
 
 /* error codes */
@@ -57,6 +57,9 @@ extern "C" {
 #define DS_OBS_RADIAL 0
 #define DS_OBS_LIDAR 1
 #define DS_OBS_VIEW_CONE 2
+/* observation buffer element types (ds_set_obs_format) */
+#define DS_OBS_F32 0
+#define DS_OBS_BF16 1
 
 /* static per-agent flags (ds_tables.sflags) */
 #define DS_SF_CONTROLLED 1
@@ -162,7 +165,7 @@ typedef struct ds_step_args {
   const double *grid_accel;  /* [n_accel] ActionGrid.accelerations (discrete mode) */
   const double *grid_steer;  /* [n_steer] ActionGrid.steerings */
   int32_t n_accel, n_steer;
-  float *obs;                /* [n_rows, obs_width] */
+  void *obs;                 /* [n_rows, row_stride] in the handle's obs format (default float32, stride obs_width) */
   float *rewards;            /* [n_rows] */
   uint8_t *dones;            /* [n_rows] */
   uint8_t *info;             /* [3, n_rows]: goal, veh_collision, offroad */
@@ -192,15 +195,33 @@ int ds_destroy(ds_handle *h);
 /* Reset the worlds whose world_mask[w] != 0 (device [n_worlds] u8; NULL = all)
  * and write their observation rows; rewards/dones rows of those worlds are
  * zeroed (engine.py:657-662). */
-int ds_reset(ds_handle *h, const uint8_t *world_mask, float *obs, float *rewards,
+int ds_reset(ds_handle *h, const uint8_t *world_mask, void *obs, float *rewards,
              uint8_t *dones, const float *obs_scale, int32_t *sel_idx,
              void *stream);
 
 int ds_step(ds_handle *h, const ds_step_args *args, void *stream);
 
 /* Recompute observations from the current state only (World.observe). */
-int ds_observe(ds_handle *h, const uint8_t *world_mask, float *obs,
+int ds_observe(ds_handle *h, const uint8_t *world_mask, void *obs,
                const float *obs_scale, int32_t *sel_idx, void *stream);
+
+/* Observation buffer format for every later ds_step / ds_reset / ds_observe
+ * of this handle: element type DS_OBS_F32 (default) or DS_OBS_BF16 and the
+ * row stride in elements (0 = obs_width; otherwise >= obs_width).  Pad
+ * columns [obs_width, row_stride) are written as zeros, so a bf16 buffer
+ * with a stride padded to a multiple of 8 feeds a policy GEMM directly
+ * (no cast, 16-B aligned rows).  The reference returns float64 rows
+ * (engine.py:603-608); VecDriveEnv divides them by the scale (env.py:121). */
+int ds_set_obs_format(ds_handle *h, int dtype, int row_stride);
+
+/* Categorical sample per row by Gumbel-max: out[r] = argmax_j(logits[r, j] +
+ * G(seed, counter, r, j)), G standard Gumbel noise from a counter-based hash
+ * (deterministic for (seed, counter)).  logits: device [rows, ld] float32
+ * (dtype DS_OBS_F32) or bfloat16 (DS_OBS_BF16), first n columns used.  The
+ * reference trainer samples torch.distributions.Categorical(logits)
+ * (ippo.py:136-142); this is the in-loop sampler of the device rollout. */
+int ds_sample_categorical(const void *logits, int dtype, int64_t rows, int32_t n, int64_t ld,
+                          uint64_t seed, uint64_t counter, int32_t *out, void *stream);
 
 /* Copy up to max_records ring entries (6 int32 each) to host memory `out`,
  * in ring order, reset the ring, and return the count in *n_out.

@@ -14,7 +14,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdrivesim_b200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
+OBS_F32, OBS_BF16 = 0, 1   # ds_set_obs_format element types
 
 DS_OK = 0
 DS_E_INVALID = -1
@@ -92,7 +93,7 @@ class DsStepArgs(C.Structure):
 
 
 EXPORTS = ["ds_abi_version", "ds_lidar_supported", "ds_struct_sizes", "ds_last_error", "ds_create", "ds_destroy", "ds_reset", "ds_step",
-           "ds_observe", "ds_episode_drain", "ds_host_hypot_libm", "ds_host_hypot_cpython",
+           "ds_observe", "ds_set_obs_format", "ds_sample_categorical", "ds_episode_drain", "ds_host_hypot_libm", "ds_host_hypot_cpython",
            "ds_host_hypot_port", "ds_host_wrap_port", "ds_host_road_headings"]
 
 _lib = None
@@ -118,6 +119,9 @@ def lib():
     L.ds_step.argtypes = [_p, C.POINTER(DsStepArgs), _p]
     L.ds_observe.argtypes = [_p, _p, _p, _p, _p, _p]
     L.ds_episode_drain.argtypes = [_p, _p, C.c_int32, C.POINTER(C.c_int32), _p]
+    L.ds_set_obs_format.argtypes = [_p, C.c_int, C.c_int]
+    L.ds_sample_categorical.argtypes = [_p, C.c_int, C.c_int64, C.c_int32, C.c_int64,
+                                        C.c_uint64, C.c_uint64, _p, _p]
     for n in ("ds_host_hypot_libm", "ds_host_hypot_cpython", "ds_host_hypot_port"):
         getattr(L, n).argtypes = [_p, _p, C.c_int64, _p]
     L.ds_host_road_headings.argtypes = [_p, _p, _p, C.c_int64, _p]

@@ -75,6 +75,8 @@ int ds_create(const ds_tables *tables, const ds_config *cfg, ds_state *state, in
   h->st = *state;
   h->device = device;
   h->obs_width = c.obs_width;
+  h->obs_dtype = DS_OBS_F32;
+  h->obs_stride = c.obs_width;
   e = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) {
     delete h;
@@ -105,7 +107,32 @@ int ds_destroy(ds_handle *h) {
   return DS_OK;
 }
 
-int ds_reset(ds_handle *h, const uint8_t *world_mask, float *obs, float *rewards, uint8_t *dones,
+int ds_set_obs_format(ds_handle *h, int dtype, int row_stride) {
+  if (!h) return fail(DS_E_INVALID, "ds_set_obs_format: null handle");
+  if (dtype != DS_OBS_F32 && dtype != DS_OBS_BF16)
+    return fail(DS_E_INVALID, "unknown observation dtype %d", dtype);
+  if (row_stride == 0) row_stride = h->obs_width;
+  if (row_stride < h->obs_width)
+    return fail(DS_E_INVALID, "row stride %d < observation width %d", row_stride, h->obs_width);
+  h->obs_dtype = dtype;
+  h->obs_stride = row_stride;
+  return DS_OK;
+}
+
+int ds_sample_categorical(const void *logits, int dtype, int64_t rows, int32_t n, int64_t ld,
+                          uint64_t seed, uint64_t counter, int32_t *out, void *stream) {
+  if (rows < 0 || n < 1 || ld < n) return fail(DS_E_INVALID, "ds_sample_categorical: bad shape");
+  if (dtype != DS_OBS_F32 && dtype != DS_OBS_BF16)
+    return fail(DS_E_INVALID, "ds_sample_categorical: unknown dtype %d", dtype);
+  if (rows == 0) return DS_OK;
+  if (!logits || !out) return fail(DS_E_INVALID, "ds_sample_categorical: null argument");
+  cudaError_t e = ds::launch_sample(logits, dtype, rows, n, ld, seed, counter, out,
+                                    (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "sample kernel");
+  return DS_OK;
+}
+
+int ds_reset(ds_handle *h, const uint8_t *world_mask, void *obs, float *rewards, uint8_t *dones,
              const float *obs_scale, int32_t *sel_idx, void *stream) {
   if (!h || !obs) return fail(DS_E_INVALID, "ds_reset: null argument");
   cudaStream_t s = (cudaStream_t)stream;
@@ -116,7 +143,7 @@ int ds_reset(ds_handle *h, const uint8_t *world_mask, float *obs, float *rewards
   return DS_OK;
 }
 
-int ds_observe(ds_handle *h, const uint8_t *world_mask, float *obs, const float *obs_scale,
+int ds_observe(ds_handle *h, const uint8_t *world_mask, void *obs, const float *obs_scale,
                int32_t *sel_idx, void *stream) {
   if (!h || !obs) return fail(DS_E_INVALID, "ds_observe: null argument");
   cudaError_t e = ds::launch_observe(h, world_mask, obs, obs_scale, sel_idx, (cudaStream_t)stream);

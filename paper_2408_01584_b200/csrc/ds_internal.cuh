@@ -18,6 +18,8 @@ struct ds_handle {
   int obs_warps;        // warps per world CTA in the observation kernel
   int obs_shared_pts;   // 1: road points staged in shared memory
   size_t obs_smem;
+  int obs_dtype;        // DS_OBS_F32 / DS_OBS_BF16
+  int obs_stride;       // elements per observation row (>= obs_width)
   uint32_t ring_read;   // host mirror of entries already drained
 };
 
@@ -29,14 +31,16 @@ constexpr int kSelCap = 128;
 cudaError_t launch_step(const ds_handle *h, const ds_step_args *a, cudaStream_t s);
 cudaError_t launch_reset(const ds_handle *h, const uint8_t *mask, float *rewards,
                          uint8_t *dones, cudaStream_t s);
-cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, float *obs,
-                           const float *inv_scale, int32_t *sel_idx, cudaStream_t s);
+cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, void *obs,
+                           const float *scale, int32_t *sel_idx, cudaStream_t s);
 void obs_plan(ds_handle *h, int max_dynamic_smem);
 size_t lidar_smem_bytes(int max_agents, int obs_width);
 int lidar_warps();
 cudaError_t configure_lidar_kernels(int max_dynamic_smem);
-cudaError_t launch_lidar(const ds_handle *h, const uint8_t *mask, float *obs, const float *scale,
+cudaError_t launch_lidar(const ds_handle *h, const uint8_t *mask, void *obs, const float *scale,
                          cudaStream_t s);
+cudaError_t launch_sample(const void *logits, int dtype, int64_t rows, int n, int64_t ld,
+                          uint64_t seed, uint64_t counter, int32_t *out, cudaStream_t s);
 size_t step_smem_bytes(int max_agents);
 cudaError_t configure_kernels(int max_dynamic_smem);
 cudaError_t configure_step_kernels(int max_dynamic_smem);

@@ -23,6 +23,7 @@
 //  * a road replaces the box hit only if strictly nearer; beyond max_range
 //    the ray reports max_range with type none.
 #include "ds_internal.cuh"
+#include "ds_obs_out.cuh"
 #include "ds_rows.cuh"
 
 namespace ds {
@@ -39,8 +40,9 @@ __host__ __device__ inline size_t lidar_agents_bytes(int amax) {
 }
 
 // per warp: ray dx, dy, box-min bits, segment-key min, limit (8 B each) + row
+// (+16 B: the staged row is shifted by up to 3 floats to the output's phase)
 __host__ __device__ inline size_t lidar_warp_bytes(int obs_width, int n_rays) {
-  return al16l((size_t)n_rays * 5 * sizeof(double) + (size_t)obs_width * sizeof(float));
+  return al16l((size_t)n_rays * 5 * sizeof(double) + (size_t)obs_width * sizeof(float) + 16);
 }
 
 constexpr double kInvTwoPi = 0.15915494309189535;
@@ -156,7 +158,7 @@ __device__ __forceinline__ double ray_box(double ox, double oy, double dx, doubl
 
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
-    ds_tables T, ds_config C, ds_state St, const uint8_t *mask, float *obs, const float *scale,
+    ds_tables T, ds_config C, ds_state St, const uint8_t *mask, const ObsOut O, const float *scale,
     int obs_width) {
   const int w = blockIdx.x;
   if (mask && !mask[w]) return;
@@ -177,7 +179,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
   double *rlim = rdy + C.n_rays;
   unsigned long long *rbest = reinterpret_cast<unsigned long long *>(rlim + C.n_rays);
   unsigned long long *rseg = rbest + C.n_rays;
-  float *row = reinterpret_cast<float *>(rseg + C.n_rays);
+  float *const row0 = reinterpret_cast<float *>(rseg + C.n_rays);
+  const int row0_phase = (int)((reinterpret_cast<uintptr_t>(row0) >> 2) & 3);
 
   const int64_t a0 = T.a_off[w];
   const int A = (int)(T.a_off[w + 1] - a0);
@@ -204,15 +207,14 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
 
   for (int r = warp; r < nrow; r += WARPS) {
     const int64_t orow = c0 + r;
-    float *out = obs + orow * (int64_t)obs_width;
     const int64_t g = T.row_agent[orow];
     const int i = (int)(g - a0);
     const uint16_t f = St.flags[g];
     if (f & (DS_F_DONE | DS_F_REMOVED)) {
-      #pragma unroll 1
-      for (int c = lane; c < obs_width; c += 32) out[c] = 0.0f;
+      zero_row(O, orow, lane);
       continue;
     }
+    float *const row = row0 + ((out_row_phase(O, orow) - row0_phase) & 3);
     const double ox = sx[i], oy = sy[i], h = St.heading[g];
     if (lane == 0) {
       // _fill_ego (obs:129-142)
@@ -397,13 +399,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
       slot[4] = type == 3 ? 1.0f : 0.0f;
     }
     __syncwarp();
-    if (scale) {
-      #pragma unroll 1
-      for (int c = lane; c < obs_width; c += 32) out[c] = row[c] / scale[c];
-    } else {
-      #pragma unroll 1
-      for (int c = lane; c < obs_width; c += 32) out[c] = row[c];
-    }
+    write_row(O, orow, row, obs_width, scale, lane);
     __syncwarp();
   }
 }
@@ -422,10 +418,11 @@ cudaError_t configure_lidar_kernels(int max_dynamic_smem) {
                               cudaFuncAttributeMaxDynamicSharedMemorySize, max_dynamic_smem);
 }
 
-cudaError_t launch_lidar(const ds_handle *h, const uint8_t *mask, float *obs, const float *scale,
+cudaError_t launch_lidar(const ds_handle *h, const uint8_t *mask, void *obs, const float *scale,
                          cudaStream_t s) {
+  const ObsOut O{obs, h->obs_dtype, h->obs_stride};
   obs_lidar_kernel<kLidarWarps><<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(
-      h->tab, h->cfg, h->st, mask, obs, scale, h->obs_width);
+      h->tab, h->cfg, h->st, mask, O, scale, h->obs_width);
   return cudaGetLastError();
 }
 

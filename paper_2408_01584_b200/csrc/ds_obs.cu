@@ -26,6 +26,7 @@
 // A set G beyond its capacity (or a key bound too loose for the bucket width)
 // falls back to the reference's serial insertion -- exact by construction.
 #include "ds_internal.cuh"
+#include "ds_obs_out.cuh"
 #include "ds_rows.cuh"
 
 namespace ds {
@@ -599,7 +600,7 @@ struct RadialK {
 
 template <int WARPS, bool SharedPts, int CAPA, int CAPR>
 __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kernel(
-    ds_tables T, ds_config C, ds_state St, const RadialK K, const uint8_t *mask, float *obs,
+    ds_tables T, ds_config C, ds_state St, const RadialK K, const uint8_t *mask, const ObsOut O,
     const float *scale, int32_t *sel_idx, int obs_width) {
   const int w = blockIdx.x;
   if (mask && !mask[w]) return;
@@ -676,27 +677,19 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
 
   for (int r = warp; r < nrow; r += WARPS) {
     const int64_t orow = c0 + r;
-    float *out = obs + orow * (int64_t)obs_width;
     const int64_t g = T.row_agent[orow];
     const int i = (int)(g - a0);
     const uint16_t f = St.flags[g];
-    // 16-B phase of the output row; the staged row copies it
-    const int out_phase = (int)((reinterpret_cast<uintptr_t>(out) >> 2) & 3);
-    const int head = (4 - out_phase) & 3;           // floats until out is 16-B aligned
-    const int nvec = obs_width > head ? (obs_width - head) >> 2 : 0;
     if (f & (DS_F_DONE | DS_F_REMOVED)) {
       // finished / removed rows are zero-filled (engine.py:502-512)
-      if (lane < head && lane < obs_width) out[lane] = 0.0f;
-      #pragma unroll 1
-      for (int v = lane; v < nvec; v += 32)
-        reinterpret_cast<float4 *>(out + head)[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-      #pragma unroll 1
-      for (int c = head + 4 * nvec + lane; c < obs_width; c += 32) out[c] = 0.0f;
+      zero_row(O, orow, lane);
       if (sel_idx)
         #pragma unroll 1
         for (int c = lane; c < sel_w; c += 32) sel_idx[orow * sel_w + c] = -1;
       continue;
     }
+    // the staged row copies the output row's 16-B phase (vector write-out)
+    const int out_phase = out_row_phase(O, orow);
     float *const row = row0 - ((row0_phase - out_phase) & 3);   // contiguous staged row
     const double px = ax[i], py = ay[i], h = ah[i];
     const double ch = ac[i], sh = as[i];
@@ -792,32 +785,8 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
       }
     }
     __syncwarp();
-    // ---- coalesced write-out of the staged row: scalar head, float4 body
-    // (the staged row has the output's 16-B phase), scalar tail
-    {
-      const float4 *rv = reinterpret_cast<const float4 *>(row + head);
-      float4 *ov = reinterpret_cast<float4 *>(out + head);
-      const int tail0 = head + 4 * nvec;
-      if (scale) {
-        if (lane < head && lane < obs_width) out[lane] = row[lane] / scale[lane];
-        #pragma unroll 1
-        for (int v = lane; v < nvec; v += 32) {
-          float4 x = rv[v];
-          const float *sc = scale + head + 4 * v;
-          x.x /= sc[0];
-          x.y /= sc[1];
-          x.z /= sc[2];
-          x.w /= sc[3];
-          ov[v] = x;
-        }
-        for (int c = tail0 + lane; c < obs_width; c += 32) out[c] = row[c] / scale[c];
-      } else {
-        if (lane < head && lane < obs_width) out[lane] = row[lane];
-        #pragma unroll 1
-        for (int v = lane; v < nvec; v += 32) ov[v] = rv[v];
-        for (int c = tail0 + lane; c < obs_width; c += 32) out[c] = row[c];
-      }
-    }
+    // ---- coalesced write-out of the staged row
+    write_row(O, orow, row, obs_width, scale, lane);
     __syncwarp();
   }
 }
@@ -856,7 +825,7 @@ void obs_plan(ds_handle *h, int max_optin) {
   }
 }
 
-cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, float *obs,
+cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, void *obs,
                            const float *scale, int32_t *sel_idx, cudaStream_t s) {
   if (h->cfg.obs_mode != DS_OBS_RADIAL) {
     if (sel_idx) return cudaErrorInvalidValue;   // selection indices are radial-only
@@ -864,6 +833,7 @@ cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, float *obs,
   }
   const bool fixed = h->cfg.max_agents_obs == 16 && h->cfg.max_road_points_obs == 64;
   const int W = h->tab.n_worlds;
+  const ObsOut O{obs, h->obs_dtype, h->obs_stride};
   RadialK K;
   K.radius = h->cfg.radius;
   K.reach = K.radius + 1e-6;
@@ -875,17 +845,17 @@ cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, float *obs,
   if (h->obs_shared_pts) {
     if (fixed)
       obs_radial_kernel<kWarpsShared, true, 16, 64><<<W, kWarpsShared * 32, h->obs_smem, s>>>(
-          h->tab, h->cfg, h->st, K, mask, obs, scale, sel_idx, h->obs_width);
+          h->tab, h->cfg, h->st, K, mask, O, scale, sel_idx, h->obs_width);
     else
       obs_radial_kernel<kWarpsShared, true, 0, 0><<<W, kWarpsShared * 32, h->obs_smem, s>>>(
-          h->tab, h->cfg, h->st, K, mask, obs, scale, sel_idx, h->obs_width);
+          h->tab, h->cfg, h->st, K, mask, O, scale, sel_idx, h->obs_width);
   } else {
     if (fixed)
       obs_radial_kernel<kWarpsGlobal, false, 16, 64><<<W, kWarpsGlobal * 32, h->obs_smem, s>>>(
-          h->tab, h->cfg, h->st, K, mask, obs, scale, sel_idx, h->obs_width);
+          h->tab, h->cfg, h->st, K, mask, O, scale, sel_idx, h->obs_width);
     else
       obs_radial_kernel<kWarpsGlobal, false, 0, 0><<<W, kWarpsGlobal * 32, h->obs_smem, s>>>(
-          h->tab, h->cfg, h->st, K, mask, obs, scale, sel_idx, h->obs_width);
+          h->tab, h->cfg, h->st, K, mask, O, scale, sel_idx, h->obs_width);
   }
   return cudaGetLastError();
 }

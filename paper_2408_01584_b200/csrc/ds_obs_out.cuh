@@ -1,0 +1,115 @@
+// ds_obs_out.cuh -- write-out of one staged observation row (shared memory,
+// float) into the caller's observation buffer in the handle's format:
+// float32 (the reference's values rounded to float32) or bfloat16 (round to
+// nearest even, the format an in-loop bf16 policy consumes), with a row
+// stride >= the observation width whose pad columns are written as zeros.
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include "ds_internal.cuh"
+
+namespace ds {
+
+struct ObsOut {
+  void *base;
+  int dtype;    // DS_OBS_F32 / DS_OBS_BF16
+  int stride;   // elements per row
+};
+
+// float phase (0..3) modulo 16 B that the staged row should have so that the
+// float32 write-out can use 16-B vector stores (bf16 rows want phase 0)
+__device__ __forceinline__ int out_row_phase(const ObsOut &o, int64_t orow) {
+  if (o.dtype != DS_OBS_F32) return 0;
+  const float *out = static_cast<const float *>(o.base) + orow * (int64_t)o.stride;
+  return (int)((reinterpret_cast<uintptr_t>(out) >> 2) & 3);
+}
+
+__device__ __forceinline__ float scaled(const float *row, const float *scale, int c) {
+  return scale ? row[c] / scale[c] : row[c];
+}
+
+// Warp-collective: row[0, width) (divided by scale[c] when scale != NULL) to
+// output row orow, zeros in [width, stride).
+__device__ __forceinline__ void write_row(const ObsOut &o, int64_t orow, const float *row,
+                                          int width, const float *scale, int lane) {
+  if (o.dtype == DS_OBS_F32) {
+    float *out = static_cast<float *>(o.base) + orow * (int64_t)o.stride;
+    const int ph = (int)((reinterpret_cast<uintptr_t>(out) >> 2) & 3);
+    const bool vec = ((reinterpret_cast<uintptr_t>(row) >> 2) & 3) == (uintptr_t)ph;
+    const int head = vec ? ((4 - ph) & 3) : width;
+    const int nvec = vec && width > head ? (width - head) >> 2 : 0;
+    const int tail0 = head < width ? head + 4 * nvec : width;
+    if (lane < head && lane < width) out[lane] = scaled(row, scale, lane);
+    const float4 *rv = reinterpret_cast<const float4 *>(row + head);
+    float4 *ov = reinterpret_cast<float4 *>(out + head);
+#pragma unroll 1
+    for (int v = lane; v < nvec; v += 32) {
+      float4 x = rv[v];
+      if (scale) {
+        const float *sc = scale + head + 4 * v;
+        x.x /= sc[0];
+        x.y /= sc[1];
+        x.z /= sc[2];
+        x.w /= sc[3];
+      }
+      ov[v] = x;
+    }
+#pragma unroll 1
+    for (int c = tail0 + lane; c < width; c += 32) out[c] = scaled(row, scale, c);
+#pragma unroll 1
+    for (int c = width + lane; c < o.stride; c += 32) out[c] = 0.0f;
+    return;
+  }
+  __nv_bfloat16 *out = static_cast<__nv_bfloat16 *>(o.base) + orow * (int64_t)o.stride;
+  const bool vec = ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(row)) & 15) == 0;
+  const int nvec = vec ? width >> 3 : 0;
+#pragma unroll 1
+  for (int v = lane; v < nvec; v += 32) {
+    float4 a = reinterpret_cast<const float4 *>(row)[2 * v];
+    float4 b = reinterpret_cast<const float4 *>(row)[2 * v + 1];
+    if (scale) {
+      const float *sc = scale + 8 * v;
+      a.x /= sc[0];
+      a.y /= sc[1];
+      a.z /= sc[2];
+      a.w /= sc[3];
+      b.x /= sc[4];
+      b.y /= sc[5];
+      b.z /= sc[6];
+      b.w /= sc[7];
+    }
+    __nv_bfloat162 q[4] = {__floats2bfloat162_rn(a.x, a.y), __floats2bfloat162_rn(a.z, a.w),
+                           __floats2bfloat162_rn(b.x, b.y), __floats2bfloat162_rn(b.z, b.w)};
+    reinterpret_cast<uint4 *>(out)[v] = *reinterpret_cast<const uint4 *>(q);
+  }
+#pragma unroll 1
+  for (int c = 8 * nvec + lane; c < width; c += 32) out[c] = __float2bfloat16_rn(scaled(row, scale, c));
+#pragma unroll 1
+  for (int c = width + lane; c < o.stride; c += 32) out[c] = __float2bfloat16_rn(0.0f);
+}
+
+// Warp-collective: a zero output row (done / removed agents, engine.py:502-512).
+__device__ __forceinline__ void zero_row(const ObsOut &o, int64_t orow, int lane) {
+  const size_t esz = o.dtype == DS_OBS_F32 ? 4 : 2;
+  unsigned char *out = static_cast<unsigned char *>(o.base) + (size_t)orow * o.stride * esz;
+  const size_t bytes = (size_t)o.stride * esz;
+  const size_t head = ((16 - (reinterpret_cast<uintptr_t>(out) & 15)) & 15) < bytes
+                          ? ((16 - (reinterpret_cast<uintptr_t>(out) & 15)) & 15)
+                          : bytes;
+  const size_t nvec = (bytes - head) >> 4;
+  // element-sized head/tail stores (the buffer is element aligned)
+  for (size_t c = lane * esz; c < head; c += 32 * esz) {
+    if (esz == 4) *reinterpret_cast<float *>(out + c) = 0.0f;
+    else *reinterpret_cast<uint16_t *>(out + c) = 0;
+  }
+#pragma unroll 1
+  for (size_t v = lane; v < nvec; v += 32)
+    reinterpret_cast<uint4 *>(out + head)[v] = make_uint4(0u, 0u, 0u, 0u);
+  for (size_t c = head + 16 * nvec + lane * esz; c < bytes; c += 32 * esz) {
+    if (esz == 4) *reinterpret_cast<float *>(out + c) = 0.0f;
+    else *reinterpret_cast<uint16_t *>(out + c) = 0;
+  }
+}
+
+}  // namespace ds

@@ -1,0 +1,87 @@
+// ds_sample.cu -- in-loop categorical action sampler of the device rollout
+// (the reference trainer samples torch.distributions.Categorical(logits),
+// pkg/rl/src/drivesim_rl/ippo.py:136-142).
+//
+// Gumbel-max: out[r] = argmax_j (logits[r, j] + G_rj), G_rj = -log(-log u_rj)
+// with u_rj in (0, 1) from a counter-based hash of (seed, counter, r, j), so a
+// rollout is reproducible from (seed, step) alone and needs no RNG state.
+// One warp per row, lanes strided over the columns, warp argmax (ties to the
+// smaller column).  One launch replaces the rand / log / log / add / argmax
+// chain of the eager torch sampler.
+#include <cuda_bf16.h>
+
+#include "ds_internal.cuh"
+
+namespace ds {
+
+namespace {
+
+constexpr int kSampleWarps = 8;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// uniform in (0, 1): 24 random bits, centred in their cell
+__device__ __forceinline__ float hash_uniform(uint64_t key, uint64_t r, uint32_t j) {
+  const uint64_t h = mix64(key ^ mix64(r * 0x9e3779b97f4a7c15ull + j));
+  return ((float)(uint32_t)(h >> 40) + 0.5f) * 5.9604644775390625e-8f;
+}
+
+template <typename T>
+__device__ __forceinline__ float load_logit(const T *p);
+template <>
+__device__ __forceinline__ float load_logit<float>(const float *p) { return *p; }
+template <>
+__device__ __forceinline__ float load_logit<__nv_bfloat16>(const __nv_bfloat16 *p) {
+  return __bfloat162float(*p);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSampleWarps * 32) sample_kernel(const T *logits, int64_t rows,
+                                                                   int n, int64_t ld,
+                                                                   uint64_t key, int32_t *out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * kSampleWarps + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const T *row = logits + r * ld;
+  float best = -INFINITY;
+  int arg = 0x7fffffff;
+  for (int j = lane; j < n; j += 32) {
+    const float u = hash_uniform(key, (uint64_t)r, (uint32_t)j);
+    const float v = load_logit(row + j) - logf(-logf(u));
+    if (v > best || (v == best && j < arg) || arg == 0x7fffffff) {
+      best = v;
+      arg = j;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, off);
+    const int oa = __shfl_xor_sync(0xffffffffu, arg, off);
+    if (ob > best || (ob == best && oa < arg)) {
+      best = ob;
+      arg = oa;
+    }
+  }
+  if (lane == 0) out[r] = arg;
+}
+
+}  // namespace
+
+cudaError_t launch_sample(const void *logits, int dtype, int64_t rows, int n, int64_t ld,
+                          uint64_t seed, uint64_t counter, int32_t *out, cudaStream_t s) {
+  const uint64_t key = mix64(seed ^ mix64(counter + 0x632be59bd9b4e019ull));
+  const int64_t blocks = (rows + kSampleWarps - 1) / kSampleWarps;
+  if (dtype == DS_OBS_BF16)
+    sample_kernel<__nv_bfloat16><<<(unsigned)blocks, kSampleWarps * 32, 0, s>>>(
+        static_cast<const __nv_bfloat16 *>(logits), rows, n, ld, key, out);
+  else
+    sample_kernel<float><<<(unsigned)blocks, kSampleWarps * 32, 0, s>>>(
+        static_cast<const float *>(logits), rows, n, ld, key, out);
+  return cudaGetLastError();
+}
+
+}  // namespace ds

@@ -419,6 +419,23 @@ class SimBatch:
                                  self._stream()), "ds_reset")
         return self.observations
 
+    def set_obs_format(self, dtype=torch.float32, row_stride: int | None = None):
+        """Observation buffer format of every later step/reset/observe:
+        float32 (default) or bfloat16, rows padded to ``row_stride`` elements
+        (pad columns read 0).  ``observations`` stays the [n, width] view of
+        the padded buffer; a bf16 buffer padded to a multiple of 8 feeds a
+        policy GEMM directly (ds_set_obs_format)."""
+        self._check_open()
+        code = {torch.float32: N.OBS_F32, torch.bfloat16: N.OBS_BF16}.get(dtype)
+        if code is None:
+            raise ValueError(f"unsupported observation dtype {dtype}")
+        stride = self.width if row_stride is None else int(row_stride)
+        N.check(N.lib().ds_set_obs_format(self._handle, code, stride), "ds_set_obs_format")
+        nc = self.n_controlled
+        self._obs_buf = torch.zeros((max(nc, 1), stride), dtype=dtype, device=self.device)
+        self.observations = self._obs_buf[:nc, :self.width]
+        return self.observations
+
     def observe(self, obs_scale=None, sel_idx=None):
         N.check(N.lib().ds_observe(self._handle, None, self.observations.data_ptr(),
                                    obs_scale.data_ptr() if obs_scale is not None else None,
@@ -549,3 +566,26 @@ def benchmark(scenarios: list, cfg: SimConfig, worlds: int, steps: int, policy: 
                            controlled_agents=batch.n_controlled)
     batch.close()
     return rep
+
+
+def sample_categorical(logits: torch.Tensor, seed: int, counter: int,
+                       out: torch.Tensor | None = None) -> torch.Tensor:
+    """One categorical sample per row of ``logits`` ([rows, n], float32 or
+    bfloat16, unit column stride, any row stride) by Gumbel-max with noise
+    from a counter-based hash of (seed, counter, row, column): the in-loop
+    sampler of the device rollout (ds_sample_categorical; the reference
+    trainer samples torch.distributions.Categorical, ippo.py:136-142)."""
+    if logits.ndim != 2 or logits.stride(1) != 1:
+        raise ValueError("logits must be 2-D with unit column stride")
+    code = {torch.float32: N.OBS_F32, torch.bfloat16: N.OBS_BF16}.get(logits.dtype)
+    if code is None:
+        raise ValueError(f"unsupported logits dtype {logits.dtype}")
+    rows, n = logits.shape
+    if out is None:
+        out = torch.empty(rows, dtype=torch.int32, device=logits.device)
+    stream = C.c_void_p(torch.cuda.current_stream(logits.device).cuda_stream)
+    N.check(N.lib().ds_sample_categorical(C.c_void_p(logits.data_ptr()), code, rows, n,
+                                          logits.stride(0), seed & (2**64 - 1),
+                                          counter & (2**64 - 1), C.c_void_p(out.data_ptr()),
+                                          stream), "ds_sample_categorical")
+    return out

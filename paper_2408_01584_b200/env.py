@@ -78,10 +78,15 @@ class EnvConfig:
     n_workers: int = 1
     device: str = "cuda"
     raw: object = None          # optional RawWorlds batch (vectorised scenes)
+    # observation buffer: "float32" (the reference's values rounded to f32) or
+    # "bfloat16" rows padded to a multiple of 8 (policy-GEMM ready, zero pad)
+    obs_dtype: str = "float32"
 
     def __post_init__(self):
         if self.rollout_length < 1:
             raise ValueError("rollout_length must be >= 1")
+        if self.obs_dtype not in ("float32", "bfloat16"):
+            raise ValueError(f"obs_dtype must be float32 or bfloat16, got {self.obs_dtype!r}")
         if self.sim is None:
             self.sim = SimConfig(collision_behavior="remove_agent")
 
@@ -146,6 +151,8 @@ class VecDriveEnv:
         self.n_agents = self.batch.n_controlled
         self.obs_width = obs_width(cfg.sim.obs)
         self.n_actions = self.grid.size
+        if cfg.obs_dtype == "bfloat16":
+            self.batch.set_obs_format(torch.bfloat16, (self.obs_width + 7) // 8 * 8)
         self._scale = (torch.tensor(obs_scale(cfg.sim), dtype=torch.float32, device=dev)
                        if cfg.normalize_obs else None)
         self._accels = torch.tensor(self.grid.accelerations, dtype=torch.float64, device=dev)
