@@ -223,6 +223,19 @@ int ds_set_obs_format(ds_handle *h, int dtype, int row_stride);
 int ds_sample_categorical(const void *logits, int dtype, int64_t rows, int32_t n, int64_t ld,
                           uint64_t seed, uint64_t counter, int32_t *out, void *stream);
 
+/* Batched polyline decimation (preprocess, scenario.py:387-411, with
+ * decimate_polyline, geometry.py:84-127): for every polyline p (points
+ * [poly_off[p], poly_off[p+1]) of the device FP64 arrays x, y) remove
+ * interior points by iterative smallest-triangle-area removal (ties: smaller
+ * index) while the minimum area is < threshold; keep[i] = 1 for survivors.
+ * Polylines with skip[p] != 0 (stop signs), fewer than 3 points, or
+ * threshold <= 0 are kept whole.  scratch: device buffer of
+ * ds_decimate_scratch_bytes(n_points) bytes, 8-byte aligned. */
+int64_t ds_decimate_scratch_bytes(int64_t n_points);
+int ds_decimate_polylines(const double *x, const double *y, const int64_t *poly_off,
+                          int64_t n_poly, const uint8_t *skip, double threshold, uint8_t *keep,
+                          void *scratch, int64_t n_points, void *stream);
+
 /* Copy up to max_records ring entries (6 int32 each) to host memory `out`,
  * in ring order, reset the ring, and return the count in *n_out.
  * Synchronises `stream`.  Returns DS_E_OVERFLOW if records were lost. */

@@ -93,7 +93,7 @@ class DsStepArgs(C.Structure):
 
 
 EXPORTS = ["ds_abi_version", "ds_lidar_supported", "ds_struct_sizes", "ds_last_error", "ds_create", "ds_destroy", "ds_reset", "ds_step",
-           "ds_observe", "ds_set_obs_format", "ds_sample_categorical", "ds_episode_drain", "ds_host_hypot_libm", "ds_host_hypot_cpython",
+           "ds_observe", "ds_set_obs_format", "ds_sample_categorical", "ds_decimate_scratch_bytes", "ds_decimate_polylines", "ds_episode_drain", "ds_host_hypot_libm", "ds_host_hypot_cpython",
            "ds_host_hypot_port", "ds_host_wrap_port", "ds_host_road_headings"]
 
 _lib = None
@@ -120,6 +120,9 @@ def lib():
     L.ds_observe.argtypes = [_p, _p, _p, _p, _p, _p]
     L.ds_episode_drain.argtypes = [_p, _p, C.c_int32, C.POINTER(C.c_int32), _p]
     L.ds_set_obs_format.argtypes = [_p, C.c_int, C.c_int]
+    L.ds_decimate_scratch_bytes.argtypes = [C.c_int64]
+    L.ds_decimate_polylines.argtypes = [_p, _p, _p, C.c_int64, _p, C.c_double, _p, _p,
+                                        C.c_int64, _p]
     L.ds_sample_categorical.argtypes = [_p, C.c_int, C.c_int64, C.c_int32, C.c_int64,
                                         C.c_uint64, C.c_uint64, _p, _p]
     for n in ("ds_host_hypot_libm", "ds_host_hypot_cpython", "ds_host_hypot_port"):
@@ -127,8 +130,10 @@ def lib():
     L.ds_host_road_headings.argtypes = [_p, _p, _p, C.c_int64, _p]
     L.ds_host_wrap_port.argtypes = [_p, C.c_int64, _p]
     for n in EXPORTS:
-        if n not in ("ds_abi_version", "ds_last_error", "ds_struct_sizes", "ds_lidar_supported"):
+        if n not in ("ds_abi_version", "ds_last_error", "ds_struct_sizes", "ds_lidar_supported",
+                     "ds_decimate_scratch_bytes"):
             getattr(L, n).restype = C.c_int
+    L.ds_decimate_scratch_bytes.restype = C.c_int64
     if L.ds_abi_version() != ABI_VERSION:
         raise ImportError("libdrivesim_b200.so ABI version mismatch; rebuild")
     sizes = (C.c_int64 * 4)()

@@ -132,6 +132,23 @@ int ds_sample_categorical(const void *logits, int dtype, int64_t rows, int32_t n
   return DS_OK;
 }
 
+int64_t ds_decimate_scratch_bytes(int64_t n_points) {
+  return n_points < 0 ? 0 : n_points * (int64_t)(2 * sizeof(int32_t) + sizeof(double));
+}
+
+int ds_decimate_polylines(const double *x, const double *y, const int64_t *poly_off,
+                          int64_t n_poly, const uint8_t *skip, double threshold, uint8_t *keep,
+                          void *scratch, int64_t n_points, void *stream) {
+  if (n_poly < 0 || n_points < 0) return fail(DS_E_INVALID, "ds_decimate_polylines: bad sizes");
+  if (n_poly == 0 || n_points == 0) return DS_OK;
+  if (!x || !y || !poly_off || !keep || !scratch)
+    return fail(DS_E_INVALID, "ds_decimate_polylines: null argument");
+  cudaError_t e = ds::launch_decimate(x, y, poly_off, n_poly, skip, threshold, keep, scratch,
+                                      n_points, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "decimate kernel");
+  return DS_OK;
+}
+
 int ds_reset(ds_handle *h, const uint8_t *world_mask, void *obs, float *rewards, uint8_t *dones,
              const float *obs_scale, int32_t *sel_idx, void *stream) {
   if (!h || !obs) return fail(DS_E_INVALID, "ds_reset: null argument");

@@ -39,6 +39,9 @@ int lidar_warps();
 cudaError_t configure_lidar_kernels(int max_dynamic_smem);
 cudaError_t launch_lidar(const ds_handle *h, const uint8_t *mask, void *obs, const float *scale,
                          cudaStream_t s);
+cudaError_t launch_decimate(const double *x, const double *y, const int64_t *poly_off,
+                            int64_t n_poly, const uint8_t *skip, double threshold, uint8_t *keep,
+                            void *scratch, int64_t n_points, cudaStream_t s);
 cudaError_t launch_sample(const void *logits, int dtype, int64_t rows, int n, int64_t ld,
                           uint64_t seed, uint64_t counter, int32_t *out, cudaStream_t s);
 size_t step_smem_bytes(int max_agents);
