@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdrivesim_b200.so")
+# DS_LIB_PATH (dev only): an alternative build of the same library, for A/B timing
+LIB_PATH = os.environ.get("DS_LIB_PATH") or os.path.join(_HERE, "libdrivesim_b200.so")
 ABI_VERSION = 2
 OBS_F32, OBS_BF16 = 0, 1   # ds_set_obs_format element types
 

@@ -35,7 +35,11 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNB = 256;       // histogram buckets
 constexpr int kCandGlobal = 640;  // buffered pass-1 candidates (global-points variant)
 constexpr int kCandShared = 224;  // (shared-points variant: hint-narrowed scans)
-constexpr int kWarpsShared = 24;
+// warps per world CTA: as many as the shared memory allows (occupancy is what
+// hides this kernel's latencies: 16 / 24 / 28 / 32 warps measured 2.82 /
+// 2.53 / 2.28 / 2.16 ms at C3); 32 fits the default caps with 10k points
+constexpr int kWarpsShared = 32;
+constexpr int kWarpsSharedSmall = 24;
 constexpr int kWarpsGlobal = 12;
 
 __host__ __device__ constexpr int kmax_of(int cap_a, int cap_r) {
@@ -55,7 +59,7 @@ __host__ __device__ constexpr size_t al16(size_t v) { return (v + 15) & ~size_t(
 // selection has produced sel_pl.  constexpr: with compile-time slot caps the
 // whole layout folds into immediate offsets off one base register.
 struct WarpLayout {
-  size_t row, hc, ca, cp, ga, ge, gid, gpl, gb, gf, sel_pl, sel_id, total;
+  size_t row, hc, ca, cp, ga, ge, gid, gpl, gb, gf, sel_pl, total;
 };
 
 __host__ __device__ constexpr WarpLayout make_layout(int cap_a, int cap_r, bool buffered) {
@@ -76,15 +80,21 @@ __host__ __device__ constexpr WarpLayout make_layout(int cap_a, int cap_r, bool 
   L.cp = al16(o + cc * sizeof(float));
   const size_t ge_end = al16(o + gc * sizeof(double));
   o = cand_end > ge_end ? cand_end : ge_end;
+  // the exact ids gid of G (phase B on) alias the pass-1 payloads cp (dead
+  // once scattered) when they fit beside ge
+  const bool gid_in_cp = ge_end <= L.cp && (size_t)gc * sizeof(int) <= (size_t)cc * sizeof(uint16_t);
   L.ga = o; o = al16(o + gc * sizeof(float));
-  L.gid = o; o = al16(o + gc * sizeof(int));
+  if (gid_in_cp) {
+    L.gid = L.cp;
+  } else {
+    L.gid = o; o = al16(o + gc * sizeof(int));
+  }
   L.gpl = o; o = al16(o + gc * sizeof(int));
   L.gb = o; o = al16(o + gc);
   L.gf = o; o = al16(o + gc);
   const size_t road_end = al16(L.hc + (size_t)cap_r * 11 * sizeof(float));
   if (o < road_end) o = road_end;
   L.sel_pl = o; o = al16(o + km * sizeof(int));
-  L.sel_id = o; o = al16(o + km * sizeof(int));
   L.total = o;
   return L;
 }
@@ -98,9 +108,9 @@ __host__ __device__ inline size_t agents_bytes(int max_agents) {
   return al16((size_t)max_agents * (8 * sizeof(double) + 1));
 }
 
-size_t obs_smem_bytes_shared(const ds_config &cfg, int max_agents, int max_points) {
+size_t obs_smem_bytes_shared(const ds_config &cfg, int max_agents, int max_points, int warps) {
   return agents_bytes(max_agents) + al16((size_t)max_points * sizeof(float2)) +
-         warp_layout(cfg, false).total * kWarpsShared;
+         warp_layout(cfg, false).total * warps;
 }
 
 size_t obs_smem_bytes_global(const ds_config &cfg, int max_agents) {
@@ -115,7 +125,7 @@ struct Sel {
   double *ge;
   int *gid, *gpl;
   uint8_t *gb, *gf;
-  int *sel_pl, *sel_id;
+  int *sel_pl;
   int gcap, ccap;
 };
 
@@ -292,7 +302,6 @@ __device__ int select_serial(const Src &src, int k, double radius, float r2hi, c
   cnt = __shfl_sync(kFull, cnt, 0);
   for (int m = lane; m < cnt; m += 32) {
     S.sel_pl[m] = S.gpl[m];
-    S.sel_id[m] = S.gid[m];
   }
   __syncwarp();
   return cnt;
@@ -614,7 +623,11 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
   const WarpLayout WL = kFixed ? kWL : warp_layout(C, !SharedPts);
   // shared memory: [per-warp scratch x WARPS][road points][agents] -- the
   // scratch and the points sit at (compile-time) constant offsets
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // lane / warp from opaque moves: the compiler keeps them in registers
+  // instead of re-reading the special registers (S2R) under register pressure
+  int lane, warp;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
+  asm volatile("shr.u32 %0, %1, 5;" : "=r"(warp) : "r"((int)threadIdx.x));
   unsigned char *wb = smem_raw + WL.total * warp;
   unsigned char *after_scratch = smem_raw + WL.total * WARPS;
   float2 *pts = reinterpret_cast<float2 *>(after_scratch);
@@ -637,7 +650,6 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
   S.gb = wb + WL.gb;
   S.gf = wb + WL.gf;
   S.sel_pl = reinterpret_cast<int *>(wb + WL.sel_pl);
-  S.sel_id = reinterpret_cast<int *>(wb + WL.sel_id);
   S.gcap = gcap_of(cap_a, cap_r);
   S.ccap = SharedPts ? kCandShared : kCandGlobal;
   float *const row0 = reinterpret_cast<float *>(wb + WL.row);
@@ -649,9 +661,9 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
     const int64_t g = a0 + i;
     ax[i] = St.x[g];
     ay[i] = St.y[g];
-    ah[i] = St.heading[g];
-    ac[i] = cos(ah[i]);
-    as[i] = sin(ah[i]);
+    const double hd = St.heading[g];
+    ah[i] = hd;
+    sincos(hd, &as[i], &ac[i]);
     av[i] = St.speed[g];
     al[i] = T.length[g];
     aw[i] = T.width[g];
@@ -794,6 +806,8 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
 cudaError_t configure_kernels(int max_dynamic_smem) {
   const void *ks[] = {(const void *)obs_radial_kernel<kWarpsShared, true, 16, 64>,
                       (const void *)obs_radial_kernel<kWarpsShared, true, 0, 0>,
+                      (const void *)obs_radial_kernel<kWarpsSharedSmall, true, 16, 64>,
+                      (const void *)obs_radial_kernel<kWarpsSharedSmall, true, 0, 0>,
                       (const void *)obs_radial_kernel<kWarpsGlobal, false, 16, 64>,
                       (const void *)obs_radial_kernel<kWarpsGlobal, false, 0, 0>};
   for (const void *k : ks) {
@@ -813,11 +827,18 @@ void obs_plan(ds_handle *h, int max_optin) {
     h->obs_smem = lidar_smem_bytes(h->tab.max_agents, h->obs_width);
     return;
   }
-  const size_t sh = obs_smem_bytes_shared(h->cfg, h->tab.max_agents, h->tab.max_points);
-  if (h->tab.gpt_xy && h->tab.grid_eps && sh <= (size_t)max_optin) {
+  const bool can = h->tab.gpt_xy && h->tab.grid_eps;
+  const size_t sh = obs_smem_bytes_shared(h->cfg, h->tab.max_agents, h->tab.max_points, kWarpsShared);
+  const size_t sh_small =
+      obs_smem_bytes_shared(h->cfg, h->tab.max_agents, h->tab.max_points, kWarpsSharedSmall);
+  if (can && sh <= (size_t)max_optin) {
     h->obs_shared_pts = 1;
     h->obs_warps = kWarpsShared;
     h->obs_smem = sh;
+  } else if (can && sh_small <= (size_t)max_optin) {
+    h->obs_shared_pts = 1;
+    h->obs_warps = kWarpsSharedSmall;
+    h->obs_smem = sh_small;
   } else {
     h->obs_shared_pts = 0;
     h->obs_warps = kWarpsGlobal;
@@ -842,13 +863,22 @@ cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, void *obs,
   K.cs = h->cfg.grid_cell;
   K.inv_cs = 1.0 / K.cs;
   K.key_e = (K.radius + 1.0) * 1.2e-7;
-  if (h->obs_shared_pts) {
+  if (h->obs_shared_pts && h->obs_warps == kWarpsShared) {
     if (fixed)
       obs_radial_kernel<kWarpsShared, true, 16, 64><<<W, kWarpsShared * 32, h->obs_smem, s>>>(
           h->tab, h->cfg, h->st, K, mask, O, scale, sel_idx, h->obs_width);
     else
       obs_radial_kernel<kWarpsShared, true, 0, 0><<<W, kWarpsShared * 32, h->obs_smem, s>>>(
           h->tab, h->cfg, h->st, K, mask, O, scale, sel_idx, h->obs_width);
+  } else if (h->obs_shared_pts) {
+    if (fixed)
+      obs_radial_kernel<kWarpsSharedSmall, true, 16, 64>
+          <<<W, kWarpsSharedSmall * 32, h->obs_smem, s>>>(h->tab, h->cfg, h->st, K, mask, O, scale,
+                                                         sel_idx, h->obs_width);
+    else
+      obs_radial_kernel<kWarpsSharedSmall, true, 0, 0>
+          <<<W, kWarpsSharedSmall * 32, h->obs_smem, s>>>(h->tab, h->cfg, h->st, K, mask, O, scale,
+                                                         sel_idx, h->obs_width);
   } else {
     if (fixed)
       obs_radial_kernel<kWarpsGlobal, false, 16, 64><<<W, kWarpsGlobal * 32, h->obs_smem, s>>>(

@@ -389,9 +389,10 @@ class SimBatch:
         a.auto_reset = 1 if auto_reset else 0
         a.serial = self._serial
         a.sel_idx = sel_idx.data_ptr() if sel_idx is not None else None
-        if events is not None:   # three torch.cuda.Event(enable_timing=True)
+        if events is not None:   # (start, after the world step, after obs): torch.cuda.Event or None
             for k, ev in enumerate(events):
-                a.events[k] = ev.cuda_event
+                if ev is not None:
+                    a.events[k] = ev.cuda_event
         N.check(N.lib().ds_step(self._handle, C.byref(a), self._stream()), "ds_step")
         self._serial += 1
         self._steps_since_drain += 1
@@ -589,3 +590,121 @@ def sample_categorical(logits: torch.Tensor, seed: int, counter: int,
                                           counter & (2**64 - 1), C.c_void_p(out.data_ptr()),
                                           stream), "ds_sample_categorical")
     return out
+
+
+@dataclass
+class HostStepResult:
+    """Host copies of one step's rewards / dones / info (pinned memory,
+    reused every ``depth`` steps).  ``wait()`` blocks until they landed."""
+    rewards: torch.Tensor
+    dones: torch.Tensor
+    info: dict
+    _event: object
+
+    def wait(self) -> "HostStepResult":
+        self._event.synchronize()
+        return self
+
+
+class HostStepper:
+    """Stepping from HOST action buffers with the host<->device copies
+    overlapped with the kernels (the e2e path of a CPU caller such as the
+    reference's trainer loop, ippo.py:173-179, which hands the batch numpy
+    actions and reads rewards / dones / info back every step).
+
+    Step t: the actions are staged in pinned memory and copied host->device on
+    a copy stream (slot t mod depth); the compute stream waits for that copy,
+    runs the world-step kernel, records an event, then the observation
+    kernel.  Rewards / dones / info are final once the world-step kernel is
+    done, so their device->host copy (a second copy stream) runs while the
+    observation kernel is still computing; the next step's world-step kernel
+    waits for it before overwriting them.  No host synchronisation per step:
+    ``step`` returns a HostStepResult whose ``wait()`` syncs on its copy only.
+    Results are identical to ``SimBatch.step`` with the same actions."""
+
+    def __init__(self, batch: SimBatch, act_dim: int | None = None, depth: int = 2,
+                 auto_reset: bool = True, obs_scale: torch.Tensor | None = None):
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        self.batch = batch
+        dev = batch.device
+        n = batch.n_controlled
+        self.act_dim = batch.cfg.action_dim if act_dim is None else act_dim
+        self.depth, self.auto_reset, self.obs_scale = depth, auto_reset, obs_scale
+        self._h2d = torch.cuda.Stream(dev)
+        self._d2h = torch.cuda.Stream(dev)
+        self._act_dev = [torch.empty((n, self.act_dim), dtype=torch.float32, device=dev)
+                         for _ in range(depth)]
+        host = lambda shape, dt: [torch.empty(shape, dtype=dt, pin_memory=True)  # noqa: E731
+                                  for _ in range(depth)]
+        self._act_pin = host((n, self.act_dim), torch.float32)
+        self._rew, self._done = host((n,), torch.float32), host((n,), torch.bool)
+        self._info = host((3, n), torch.bool)
+        main = torch.cuda.current_stream(dev)
+        ev = lambda: [torch.cuda.Event() for _ in range(depth)]   # noqa: E731
+        self._ev_h2d, self._ev_stepk, self._ev_d2h, self._ev_used = ev(), ev(), ev(), ev()
+        for e in self._ev_h2d + self._ev_stepk + self._ev_d2h + self._ev_used:
+            e.record(main)    # materialise the CUDA events (ds_step records raw handles)
+        self._pending = [False] * depth
+        self._t = 0
+
+    def step(self, actions) -> HostStepResult:
+        """actions: host [n_controlled, act_dim] (numpy or CPU tensor; a
+        pinned float32 tensor is copied from directly)."""
+        b = self.batch
+        k = self._t % self.depth
+        a = torch.as_tensor(actions)
+        if a.device.type != "cpu":
+            raise ValueError("HostStepper.step takes host actions; use SimBatch.step for "
+                             "device tensors")
+        if a.ndim != 2 or a.shape[0] != b.n_controlled:
+            raise ActionCountMismatch(
+                f"expected {b.n_controlled} action rows, got {a.shape[0] if a.ndim else 0}")
+        if a.shape[1] != self.act_dim:
+            raise ValueError(f"expected {self.act_dim} action columns, got {a.shape[1]}")
+        if self._pending[k]:
+            # slot k's previous step: its action copy and result copy are done
+            # before the pinned buffers are reused (the caller has had
+            # depth - 1 steps to read that result)
+            self._ev_d2h[k].synchronize()
+        direct = a.dtype == torch.float32 and a.is_contiguous() and a.is_pinned()
+        src = a if direct else self._act_pin[k]
+        if not direct:
+            src.copy_(a)
+        main = torch.cuda.current_stream(b.device)
+        with torch.cuda.stream(self._h2d):
+            # the device slot was last read by step t - depth's kernels
+            self._h2d.wait_event(self._ev_used[k])
+            self._act_dev[k].copy_(src, non_blocking=True)
+            self._ev_h2d[k].record(self._h2d)
+        main.wait_event(self._ev_h2d[k])
+        if self._t > 0:
+            # the previous step's results must be read out before this step's
+            # world-step kernel overwrites them
+            main.wait_event(self._ev_d2h[(self._t - 1) % self.depth])
+        b.step(self._act_dev[k], obs_scale=self.obs_scale, auto_reset=self.auto_reset,
+               events=(None, self._ev_stepk[k], None))
+        self._ev_used[k].record(main)
+        with torch.cuda.stream(self._d2h):
+            self._d2h.wait_event(self._ev_stepk[k])
+            self._rew[k].copy_(b.rewards, non_blocking=True)
+            self._done[k].copy_(b.dones, non_blocking=True)
+            self._info[k].copy_(b._info[:, :b.n_controlled], non_blocking=True)
+            self._ev_d2h[k].record(self._d2h)
+        self._pending[k] = True
+        self._t += 1
+        info = {key: self._info[k][i] for i, key in enumerate(("goal", "veh_collision", "offroad"))}
+        return HostStepResult(self._rew[k], self._done[k], info, self._ev_d2h[k])
+
+    @property
+    def h2d_bytes_per_step(self) -> int:
+        return self.batch.n_controlled * self.act_dim * 4
+
+    @property
+    def d2h_bytes_per_step(self) -> int:
+        return self.batch.n_controlled * (4 + 1 + 3)
+
+    def synchronize(self):
+        for k in range(self.depth):
+            if self._pending[k]:
+                self._ev_d2h[k].synchronize()
