@@ -39,10 +39,13 @@ __host__ __device__ inline size_t lidar_agents_bytes(int amax) {
   return al16l((size_t)amax * (7 * sizeof(double) + 1));
 }
 
-// per warp: ray dx, dy, box-min bits, segment-key min, limit (8 B each) + row
-// (+16 B: the staged row is shifted by up to 3 floats to the output's phase)
+// per warp: ray dx, dy, box-min bits, segment-key min, limit (8 B each), the
+// segment batch (4 f64 + edge flag per lane) + row (+16 B: the staged row is
+// shifted by up to 3 floats to the output's phase)
+constexpr size_t kSegCacheBytes = 32 * (4 * sizeof(double) + 1);
 __host__ __device__ inline size_t lidar_warp_bytes(int obs_width, int n_rays) {
-  return al16l((size_t)n_rays * 5 * sizeof(double) + (size_t)obs_width * sizeof(float) + 16);
+  return al16l((size_t)n_rays * 5 * sizeof(double) + al16l(kSegCacheBytes) +
+               (size_t)obs_width * sizeof(float) + 16);
 }
 
 constexpr double kInvTwoPi = 0.15915494309189535;
@@ -94,6 +97,16 @@ __device__ __forceinline__ void ray_range(float rel, float span, bool full, int 
   }
   k_lo = lo;
   k_hi = hi;
+}
+
+// Chebyshev ring of cell q in ring-major order (ring r >= 1 holds
+// q in [(2r - 1)^2, (2r + 1)^2))
+__device__ __forceinline__ int ring_of(int q) {
+  if (q <= 0) return 0;
+  int s = (int)sqrtf((float)q);
+  while (s * s > q) --s;
+  while ((s + 1) * (s + 1) <= q) ++s;
+  return (s + 1) >> 1;
 }
 
 // current upper bound of ray k's road search: the box hit / max_range limit
@@ -179,7 +192,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
   double *rlim = rdy + C.n_rays;
   unsigned long long *rbest = reinterpret_cast<unsigned long long *>(rlim + C.n_rays);
   unsigned long long *rseg = rbest + C.n_rays;
-  float *const row0 = reinterpret_cast<float *>(rseg + C.n_rays);
+  double *seg_ax = reinterpret_cast<double *>(rseg + C.n_rays);
+  double *seg_ay = seg_ax + 32, *seg_bx = seg_ax + 64, *seg_by = seg_ax + 96;
+  uint8_t *seg_ne = reinterpret_cast<uint8_t *>(seg_ax + 128);
+  float *const row0 = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(seg_ax) +
+                                                al16l(kSegCacheBytes));
   const int row0_phase = (int)((reinterpret_cast<uintptr_t>(row0) >> 2) & 3);
 
   const int64_t a0 = T.a_off[w];
@@ -244,28 +261,42 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
     __syncwarp();
     // boxes, box-major: the reference's candidates (visible, not ego, within
     // max_range + circumradius), each tested exactly only against the rays
-    // of a conservative angular interval around its bounding circle
-    for (int j = lane; j < A; j += 32) {
-      if (j == i || !svis[j]) continue;
-      // float superset of the candidates: a box whose centre is farther
-      // than max_range + circumradius cannot be hit within max_range
-      const float cx = (float)(sx[j] - ox), cy = (float)(sy[j] - oy);
-      const float cr = (float)scr[j] + 1e-3f;
-      const float d2 = cx * cx + cy * cy, lim = (float)max_range + cr + 1e-3f;
-      if (d2 > lim * lim) continue;
-      int k_lo = 0, k_hi = R - 1;
-      const float dist = sqrtf(d2);
-      if (dist > cr + 1e-3f) {
-        const float half = asinf(fminf(1.0f, cr / dist)) + 1e-4f;
-        float rel = fast_atan2(cy, cx) - half - fcenter;
-        rel -= (float)kTwoPi * floorf(rel * (float)kInvTwoPi);   // [0, 2pi)
-        ray_range(rel, 2.0f * half, full_circle, R, C.fov, k_lo, k_hi);
+    // of a conservative angular interval around its bounding circle; the
+    // (box, ray) pairs of 32 boxes are flattened into full warp batches
+    for (int j0 = 0; j0 < A; j0 += 32) {
+      const int j = j0 + lane;
+      int k_lo = 0, n_k = 0;
+      if (j < A && j != i && svis[j]) {
+        // float superset of the candidates: a box whose centre is farther
+        // than max_range + circumradius cannot be hit within max_range
+        const float cx = (float)(sx[j] - ox), cy = (float)(sy[j] - oy);
+        const float cr = (float)scr[j] + 1e-3f;
+        const float d2 = cx * cx + cy * cy, lim = (float)max_range + cr + 1e-3f;
+        if (d2 <= lim * lim) {
+          int k_hi = R - 1;
+          const float dist = sqrtf(d2);
+          if (dist > cr + 1e-3f) {
+            const float half = asinf(fminf(1.0f, cr / dist)) + 1e-4f;
+            float rel = fast_atan2(cy, cx) - half - fcenter;
+            rel -= (float)kTwoPi * floorf(rel * (float)kInvTwoPi);   // [0, 2pi)
+            ray_range(rel, 2.0f * half, full_circle, R, C.fov, k_lo, k_hi);
+          }
+          n_k = k_hi - k_lo + 1 > 0 ? k_hi - k_lo + 1 : 0;
+        }
       }
-      for (int m = k_lo; m <= k_hi; ++m) {
-        const int k = m >= R ? m - R : m;
-        const double d = ray_box(ox, oy, rdx[k], rdy[k], sx[j], sy[j], sc[j], ss[j], shl[j], shw[j]);
-        if (d != INFINITY)   // d >= 0; + 0.0 maps -0 to +0 so the bit order is the value order
-          atomicMin(&rbest[k], (unsigned long long)__double_as_longlong(d + 0.0));
+      FlatRows pairs;
+      pairs.build(k_lo, n_k, lane);
+      for (int p0 = 0; p0 < pairs.total; p0 += 32) {
+        int owner;
+        const int m = pairs.map_owner(p0, lane, owner);
+        const int jj = j0 + owner;
+        if (p0 + lane < pairs.total) {
+          const int k = m >= R ? m - R : m;
+          const double d = ray_box(ox, oy, rdx[k], rdy[k], sx[jj], sy[jj], sc[jj], ss[jj], shl[jj],
+                                   shw[jj]);
+          if (d != INFINITY)   // d >= 0; + 0.0 maps -0 to +0 so the bit order is the value order
+            atomicMin(&rbest[k], (unsigned long long)__double_as_longlong(d + 0.0));
+        }
       }
     }
     __syncwarp();
@@ -277,71 +308,80 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
     }
     __syncwarp();
     // road segments, segment-major, grid cells in Chebyshev rings around the
-    // origin's cell (nearest first); a cell of ring >= 2 is skipped when every
-    // ray of its angular span already has a hit nearer than the cell, and the
-    // walk stops once no ray can still be improved by the remaining rings
+    // origin's cell, nearest first, 32 cells per batch in ring-major order; a
+    // cell of ring >= 2 is skipped when every ray of its angular span already
+    // has a hit nearer than the cell, and the walk stops once no ray can
+    // still be improved by the remaining cells.  The segments of the kept
+    // cells are flattened into full warp batches, and their (segment, ray)
+    // pairs again (the segment batch is staged per warp in shared memory)
     {
       const double inv_cs = 1.0 / cs;
       const int ocx = (int)fmin(fmax(floor((ox - gx0) * inv_cs), -1e6), 1e6);
       const int ocy = (int)fmin(fmax(floor((oy - gy0) * inv_cs), -1e6), 1e6);
       const double reach = max_range + 1e-6;
       const int rmax = (int)ceil(reach * inv_cs) + 1;
+      const int n_cells = (2 * rmax + 1) * (2 * rmax + 1);
       const float cell_rad = (float)(cs * 0.7071067811865476) + 1e-3f;
-      for (int ring = 0; ring <= rmax; ++ring) {
-        const int ncell = ring == 0 ? 1 : 8 * ring;
-        for (int q0 = 0; q0 < ncell; q0 += 32) {
-          const int q = q0 + lane;
-          int sb = 0, cnt = 0;
-          if (q < ncell) {
-            int ix = ocx, iy = ocy;
-            if (ring > 0) {
-              const int side = q / (2 * ring), pos = q - side * 2 * ring;
-              if (side == 0) { ix = ocx - ring + pos; iy = ocy - ring; }
-              else if (side == 1) { ix = ocx + ring; iy = ocy - ring + pos; }
-              else if (side == 2) { ix = ocx + ring - pos; iy = ocy + ring; }
-              else { ix = ocx - ring; iy = ocy + ring - pos; }
+      for (int q0 = 0; q0 < n_cells; q0 += 32) {
+        const int q = q0 + lane;
+        int sb = 0, cnt = 0;
+        if (q < n_cells) {
+          const int ring = ring_of(q);
+          int ix = ocx, iy = ocy;
+          if (ring > 0) {
+            const int pos = q - (2 * ring - 1) * (2 * ring - 1);
+            const int side = pos / (2 * ring), along = pos - side * 2 * ring;
+            if (side == 0) { ix = ocx - ring + along; iy = ocy - ring; }
+            else if (side == 1) { ix = ocx + ring; iy = ocy - ring + along; }
+            else if (side == 2) { ix = ocx + ring - along; iy = ocy + ring; }
+            else { ix = ocx - ring; iy = ocy + ring - along; }
+          }
+          if (ix >= 0 && ix < gnx && iy >= 0 && iy < gny) {
+            const double xlo = gx0 + ix * cs, ylo = gy0 + iy * cs;
+            const double ddx = fmax(fmax(xlo - ox, ox - (xlo + cs)), 0.0);
+            const double ddy = fmax(fmax(ylo - oy, oy - (ylo + cs)), 0.0);
+            const double dmin = sqrt(ddx * ddx + ddy * ddy);
+            bool keep = dmin <= reach;
+            if (keep && ring >= 2) {
+              // bounding-circle angular span of the cell (ring >= 2: the
+              // origin is at least 1.5 cells from the cell centre)
+              const float ccx = (float)(xlo + 0.5 * cs - ox), ccy = (float)(ylo + 0.5 * cs - oy);
+              const float dc = sqrtf(ccx * ccx + ccy * ccy);
+              const float half = asinf(fminf(1.0f, cell_rad / dc)) + 1e-4f;
+              float rel = fast_atan2(ccy, ccx) - half - fcenter;
+              rel -= (float)kTwoPi * floorf(rel * (float)kInvTwoPi);
+              int k_lo, k_hi;
+              ray_range(rel, 2.0f * half, full_circle, R, C.fov, k_lo, k_hi);
+              const double need = dmin - 1e-6;
+              keep = false;
+              for (int m = k_lo; m <= k_hi && !keep; ++m) {
+                const int k = m >= R ? m - R : m;
+                keep = !(ray_bound(rlim[k], rseg[k]) < need);
+              }
             }
-            if (ix >= 0 && ix < gnx && iy >= 0 && iy < gny) {
-              const double xlo = gx0 + ix * cs, ylo = gy0 + iy * cs;
-              const double ddx = fmax(fmax(xlo - ox, ox - (xlo + cs)), 0.0);
-              const double ddy = fmax(fmax(ylo - oy, oy - (ylo + cs)), 0.0);
-              const double dmin = sqrt(ddx * ddx + ddy * ddy);
-              bool keep = dmin <= reach;
-              if (keep && ring >= 2) {
-                // bounding-circle angular span of the cell (ring >= 2: the
-                // origin is at least 1.5 cells from the cell centre)
-                const float ccx = (float)(xlo + 0.5 * cs - ox), ccy = (float)(ylo + 0.5 * cs - oy);
-                const float dc = sqrtf(ccx * ccx + ccy * ccy);
-                const float half = asinf(fminf(1.0f, cell_rad / dc)) + 1e-4f;
-                float rel = fast_atan2(ccy, ccx) - half - fcenter;
-                rel -= (float)kTwoPi * floorf(rel * (float)kInvTwoPi);
-                int k_lo, k_hi;
-                ray_range(rel, 2.0f * half, full_circle, R, C.fov, k_lo, k_hi);
-                const double need = dmin - 1e-6;
-                keep = false;
-                for (int m = k_lo; m <= k_hi && !keep; ++m) {
-                  const int k = m >= R ? m - R : m;
-                  keep = !(ray_bound(rlim[k], rseg[k]) < need);
-                }
-              }
-              if (keep) {
-                const int *c = T.aseg_cell_start + cbase + (int64_t)iy * gnx + ix;
-                sb = c[0];
-                cnt = c[1] - sb;
-              }
+            if (keep) {
+              const int *c = T.aseg_cell_start + cbase + (int64_t)iy * gnx + ix;
+              sb = c[0];
+              cnt = c[1] - sb;
             }
           }
-          FlatRows cells;
-          cells.build(sb, cnt, lane);
-          for (int f0 = 0; f0 < cells.total; f0 += 32) {
-            const int e = cells.map(f0, lane);
-            if (f0 + lane >= cells.total) continue;
+        }
+        FlatRows cells;
+        cells.build(sb, cnt, lane);
+        for (int f0 = 0; f0 < cells.total; f0 += 32) {
+          const int e = cells.map(f0, lane);
+          int k_lo = 0, n_k = 0;
+          if (f0 + lane < cells.total) {
             const double ax = T.aseg_ax[e], ay = T.aseg_ay[e], bx = T.aseg_bx[e], by = T.aseg_by[e];
-            const unsigned long long not_edge = T.aseg_edge[e] ? 0ull : 1ull;
+            seg_ax[lane] = ax;
+            seg_ay[lane] = ay;
+            seg_bx[lane] = bx;
+            seg_by[lane] = by;
+            seg_ne[lane] = T.aseg_edge[e] ? 0 : 1;
             // angular span of the segment seen from the origin (float, widened)
             const float fax = (float)(ax - ox), fay = (float)(ay - oy);
             const float fbx = (float)(bx - ox), fby = (float)(by - oy);
-            int k_lo = 0, k_hi = R - 1;
+            int k_hi = R - 1;
             if (fminf(fax * fax + fay * fay, fbx * fbx + fby * fby) > 1.0f) {
               const float pa = fast_atan2(fay, fax), pb = fast_atan2(fby, fbx);
               float dlt = pb - pa;
@@ -353,20 +393,32 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
                 ray_range(rel, fabsf(dlt) + 2e-4f, full_circle, R, C.fov, k_lo, k_hi);
               }
             }
-            for (int m = k_lo; m <= k_hi; ++m) {
+            n_k = k_hi - k_lo + 1 > 0 ? k_hi - k_lo + 1 : 0;
+          }
+          __syncwarp();
+          FlatRows pairs;
+          pairs.build(k_lo, n_k, lane);
+          for (int p0 = 0; p0 < pairs.total; p0 += 32) {
+            int owner;
+            const int m = pairs.map_owner(p0, lane, owner);
+            if (p0 + lane < pairs.total) {
               const int k = m >= R ? m - R : m;
               const double lim = rlim[k];
               const double beat = ray_bound(lim, rseg[k]);
-              const double t = ray_segment(ox, oy, rdx[k], rdy[k], ax, ay, bx, by, beat);
+              const double t = ray_segment(ox, oy, rdx[k], rdy[k], seg_ax[owner], seg_ay[owner],
+                                           seg_bx[owner], seg_by[owner], beat);
               if (t <= lim)
-                atomicMin(&rseg[k], ((unsigned long long)__double_as_longlong(t + 0.0) << 1) | not_edge);
+                atomicMin(&rseg[k], ((unsigned long long)__double_as_longlong(t + 0.0) << 1) |
+                                        (unsigned long long)seg_ne[owner]);
             }
           }
+          __syncwarp();
         }
-        __syncwarp();
-        // rings beyond `ring` lie at least ring * cs from the origin
-        if (ring >= 1) {
-          const double far = ring * cs - 1e-6;
+        // the remaining cells lie in rings >= ring_of(q0 + 32), at least
+        // (that ring - 1) cells from the origin's cell
+        const int rrem = q0 + 32 < n_cells ? ring_of(q0 + 32) : 0;
+        if (rrem >= 2) {
+          const double far = (rrem - 1) * cs - 1e-6;
           bool open = false;
           #pragma unroll 1
           for (int k = lane; k < R; k += 32) open = open || !(ray_bound(rlim[k], rseg[k]) < far);

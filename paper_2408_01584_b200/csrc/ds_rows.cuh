@@ -57,11 +57,11 @@ struct RowGeo {
 // number of row ends inside (f0, f0 + o]: one OR-reduction of end offsets
 // and a popcount (ends are distinct because empty rows were dropped).
 struct FlatRows {
-  int sb, cnt, pe, nr, total;
+  int sb, cnt, pe, nr, total, src;
   __device__ __forceinline__ void build(int sb_in, int cnt_in, int lane) {
     const unsigned bal = __ballot_sync(kFullMask, cnt_in > 0);
     nr = __popc(bal);
-    int src = (int)__fns(bal, 0, lane + 1);
+    src = (int)__fns(bal, 0, lane + 1);
     src = (src >= 0 && src < 32) ? src : 0;
     sb = __shfl_sync(kFullMask, sb_in, src);
     cnt = __shfl_sync(kFullMask, cnt_in, src);
@@ -84,6 +84,19 @@ struct FlatRows {
     const int rs = __shfl_sync(kFullMask, sb, r);
     const int rpe = __shfl_sync(kFullMask, pe, r);
     const int rc = __shfl_sync(kFullMask, cnt, r);
+    return rs + (f0 + lane - (rpe - rc));
+  }
+  // as map(), also returning the original lane that owned the range
+  __device__ __forceinline__ int map_owner(int f0, int lane, int &owner) const {
+    const bool live = lane < nr;
+    const int r0 = __popc(__ballot_sync(kFullMask, live && pe <= f0));
+    const int off = pe - f0;
+    const unsigned E = __reduce_or_sync(kFullMask, (live && off > 0 && off < 32) ? (1u << off) : 0u);
+    const int r = (r0 + __popc(E & ((2u << lane) - 1u))) & 31;
+    const int rs = __shfl_sync(kFullMask, sb, r);
+    const int rpe = __shfl_sync(kFullMask, pe, r);
+    const int rc = __shfl_sync(kFullMask, cnt, r);
+    owner = __shfl_sync(kFullMask, src, r);
     return rs + (f0 + lane - (rpe - rc));
   }
 };

@@ -140,6 +140,15 @@ def test_ragged_batch_lidar_parity():
     run_free(None, raw=ragged_batch(seed=4, num_steps=30), cfg=cfg, steps=30)
 
 
+def test_lidar_c4_shape_parity():
+    """BASELINE config 4 shape (128 agents, 10k points, 64 rays, 50 m) on two
+    worlds: the grid-ring / occlusion-culled kernel against the oracle's
+    brute force over all boxes and segments."""
+    cfg = SimConfig(init_mode="all_valid", obs=ObsConfig(mode="lidar", n_rays=64, max_range=50.0))
+    raw = generate(WaymoSpec(n_worlds=2, n_agents=128, n_points=10000, seed=21))
+    run_free(None, raw=raw, cfg=cfg, steps=12)
+
+
 def test_view_cone_parity_with_head_rotation():
     cfg = SimConfig(init_mode="all_valid", collision_behavior="remove_agent",
                     obs=ObsConfig(mode="view_cone", n_rays=17, fov=2.5, max_range=70.0))

@@ -1,12 +1,12 @@
 """Per-source-line instruction counts of one ncu report, aggregated over line
 ranges given as name=lo-hi (file ds_obs.cu unless file:lo-hi)."""
-import csv, io, subprocess, sys
+import csv, io, os, subprocess, sys
 rep = sys.argv[1]
 per_agent = float(sys.argv[2])
 ranges = []
 for spec in sys.argv[3:]:
     name, rng = spec.split("=")
-    f = "ds_obs.cu"
+    f = os.environ.get("NCU_FILE", "ds_obs.cu")
     if ":" in rng:
         f, rng = rng.split(":")
     lo, hi = rng.split("-")
