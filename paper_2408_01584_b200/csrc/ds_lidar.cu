@@ -109,6 +109,53 @@ __device__ __forceinline__ int ring_of(int q) {
   return (s + 1) >> 1;
 }
 
+// Cell offsets (dx, dy) from the origin's cell in ring-major order, for
+// rings <= kRingTableR (the grid walk reads them instead of recomputing the
+// ring / side / position of every cell)
+constexpr int kRingTableR = 20;
+constexpr int kRingTableN = (2 * kRingTableR + 1) * (2 * kRingTableR + 1);
+struct RingTable {
+  signed char d[kRingTableN][2];
+};
+constexpr RingTable make_ring_table() {
+  RingTable t{};
+  int q = 1;
+  for (int r = 1; r <= kRingTableR; ++r) {
+    for (int pos = 0; pos < 8 * r; ++pos, ++q) {
+      const int side = pos / (2 * r), along = pos - side * 2 * r;
+      int dx = 0, dy = 0;
+      if (side == 0) { dx = -r + along; dy = -r; }
+      else if (side == 1) { dx = r; dy = -r + along; }
+      else if (side == 2) { dx = r - along; dy = r; }
+      else { dx = -r; dy = r - along; }
+      t.d[q][0] = (signed char)dx;
+      t.d[q][1] = (signed char)dy;
+    }
+  }
+  return t;
+}
+__device__ RingTable g_ring_cells = make_ring_table();
+
+__device__ __forceinline__ void ring_cell(int q, bool table, int &dx, int &dy, int &ring) {
+  if (table) {
+    const char2 d = __ldg(reinterpret_cast<const char2 *>(g_ring_cells.d) + q);
+    dx = d.x;
+    dy = d.y;
+    ring = max(abs(dx), abs(dy));
+    return;
+  }
+  ring = ring_of(q);
+  dx = dy = 0;
+  if (ring > 0) {
+    const int pos = q - (2 * ring - 1) * (2 * ring - 1);
+    const int side = pos / (2 * ring), along = pos - side * 2 * ring;
+    if (side == 0) { dx = -ring + along; dy = -ring; }
+    else if (side == 1) { dx = ring; dy = -ring + along; }
+    else if (side == 2) { dx = ring - along; dy = ring; }
+    else { dx = -ring; dy = ring - along; }
+  }
+}
+
 // current upper bound of ray k's road search: the box hit / max_range limit
 // or the best segment so far (an unset key decodes to NaN, ignored by fmin)
 __device__ __forceinline__ double ray_bound(double lim, unsigned long long seg_key) {
@@ -322,37 +369,36 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
       const int rmax = (int)ceil(reach * inv_cs) + 1;
       const int n_cells = (2 * rmax + 1) * (2 * rmax + 1);
       const float cell_rad = (float)(cs * 0.7071067811865476) + 1e-3f;
+      const bool table = rmax <= kRingTableR;
+      // cell culling in float relative to the grid origin: |error| of the
+      // cell distances < 1e-4 m here, absorbed by a 2e-3 m margin (culling
+      // only ever keeps a superset of the cells that can hold a hit)
+      const float fox = (float)(ox - gx0), foy = (float)(oy - gy0), fcs = (float)cs;
+      const float freach = (float)reach;
       for (int q0 = 0; q0 < n_cells; q0 += 32) {
         const int q = q0 + lane;
         int sb = 0, cnt = 0;
         if (q < n_cells) {
-          const int ring = ring_of(q);
-          int ix = ocx, iy = ocy;
-          if (ring > 0) {
-            const int pos = q - (2 * ring - 1) * (2 * ring - 1);
-            const int side = pos / (2 * ring), along = pos - side * 2 * ring;
-            if (side == 0) { ix = ocx - ring + along; iy = ocy - ring; }
-            else if (side == 1) { ix = ocx + ring; iy = ocy - ring + along; }
-            else if (side == 2) { ix = ocx + ring - along; iy = ocy + ring; }
-            else { ix = ocx - ring; iy = ocy + ring - along; }
-          }
+          int dxc, dyc, ring;
+          ring_cell(q, table, dxc, dyc, ring);
+          const int ix = ocx + dxc, iy = ocy + dyc;
           if (ix >= 0 && ix < gnx && iy >= 0 && iy < gny) {
-            const double xlo = gx0 + ix * cs, ylo = gy0 + iy * cs;
-            const double ddx = fmax(fmax(xlo - ox, ox - (xlo + cs)), 0.0);
-            const double ddy = fmax(fmax(ylo - oy, oy - (ylo + cs)), 0.0);
-            const double dmin = sqrt(ddx * ddx + ddy * ddy);
-            bool keep = dmin <= reach;
+            const float xlo = (float)ix * fcs, ylo = (float)iy * fcs;
+            const float ddx = fmaxf(fmaxf(xlo - fox, fox - (xlo + fcs)), 0.0f);
+            const float ddy = fmaxf(fmaxf(ylo - foy, foy - (ylo + fcs)), 0.0f);
+            const float dmin = sqrtf(ddx * ddx + ddy * ddy) - 2e-3f;
+            bool keep = dmin <= freach;
             if (keep && ring >= 2) {
               // bounding-circle angular span of the cell (ring >= 2: the
               // origin is at least 1.5 cells from the cell centre)
-              const float ccx = (float)(xlo + 0.5 * cs - ox), ccy = (float)(ylo + 0.5 * cs - oy);
+              const float ccx = xlo + 0.5f * fcs - fox, ccy = ylo + 0.5f * fcs - foy;
               const float dc = sqrtf(ccx * ccx + ccy * ccy);
               const float half = asinf(fminf(1.0f, cell_rad / dc)) + 1e-4f;
               float rel = fast_atan2(ccy, ccx) - half - fcenter;
               rel -= (float)kTwoPi * floorf(rel * (float)kInvTwoPi);
               int k_lo, k_hi;
               ray_range(rel, 2.0f * half, full_circle, R, C.fov, k_lo, k_hi);
-              const double need = dmin - 1e-6;
+              const double need = (double)dmin;
               keep = false;
               for (int m = k_lo; m <= k_hi && !keep; ++m) {
                 const int k = m >= R ? m - R : m;
@@ -416,7 +462,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
         }
         // the remaining cells lie in rings >= ring_of(q0 + 32), at least
         // (that ring - 1) cells from the origin's cell
-        const int rrem = q0 + 32 < n_cells ? ring_of(q0 + 32) : 0;
+        int rrem = 0;
+        if (q0 + 32 < n_cells) {
+          int dxr, dyr;
+          ring_cell(q0 + 32, table, dxr, dyr, rrem);
+        }
         if (rrem >= 2) {
           const double far = (rrem - 1) * cs - 1e-6;
           bool open = false;
