@@ -189,7 +189,7 @@ struct RoadSrcShared {
   FlatRows rows;
   __device__ __forceinline__ void cover(double rho, int lane) {
     int b, c;
-    geo->range(rho, lane, b, c);
+    geo->range((float)rho, lane, b, c);
     rows.build(b - p0, c, lane);
   }
   __device__ __forceinline__ void restrict_to(double rho, int lane) { cover(rho, lane); }
@@ -227,7 +227,7 @@ struct RoadSrcGlobal {
   FlatRows rows;
   __device__ __forceinline__ void cover(double rho, int lane) {
     int b, c;
-    geo->range(rho, lane, b, c);
+    geo->range((float)rho, lane, b, c);
     rows.build(b, c, lane);
   }
   __device__ __forceinline__ void restrict_to(double rho, int lane) { cover(rho, lane); }
@@ -752,11 +752,11 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
       rho_hint = (double)hint.x + sqrt(mx * mx + my * my) + 1e-3;
     }
     if (cap_r > 0) {
-      RowGeo geo{T.pt_cell_start + cbase, px, py, gx0, gy0, cs, inv_cs, nx, ny, 0, 0};
-      geo.init(reach);
+      const double rx = px - gx0, ry = py - gy0;
+      const float prx = (float)rx, pry = (float)ry;
+      RowGeo geo{T.pt_cell_start + cbase, prx, pry, (float)cs, (float)inv_cs, 0.0f, nx, ny, 0, 0};
+      geo.init((float)reach);
       if (SharedPts) {
-        const double rx = px - gx0, ry = py - gy0;
-        const float prx = (float)rx, pry = (float)ry;
         // key bound: |dx_f - dx| <= E; |a - d^2| <= 4 (r + 1) E + 2 E^2 + fl32 rounding
         const double E = eps_p + fmax(fabs((double)prx - rx), fabs((double)pry - ry)) + K.key_e;
         const double D = 4.0 * (radius + 1.0) * E + 2.0 * E * E + D_fp64;

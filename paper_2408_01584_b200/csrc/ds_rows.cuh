@@ -14,37 +14,49 @@ __device__ __forceinline__ int clampi(double f, int lo, int hi) {
   return (int)f;
 }
 
-// Cell rows of a query disc around (px, py): lane l owns row iy0 + l; the
-// covered cells of a row are one contiguous range of the cell-sorted points.
+__device__ __forceinline__ int clampf(float f, int lo, int hi) {
+  if (f < (float)lo) return lo;
+  if (f > (float)hi) return hi;
+  return (int)f;
+}
+
+// Cell rows of a query disc around (px, py) -- float coordinates relative to
+// the grid origin: lane l owns row iy0 + l; the covered cells of a row are
+// one contiguous range of the cell-sorted points.  The float arithmetic is
+// widened by `marg` (>= 1 mm, far above its rounding error), so the cells
+// returned are a superset of those the exact disc touches.
 struct RowGeo {
   const int *cell_start;   // world's cell CSR (absolute point indices)
-  double px, py, gx0, gy0, cs, inv_cs;
+  float px, py, cs, inv_cs, marg;
   int nx, ny, iy0, nrows;
-  __device__ __forceinline__ void init(double reach) {
-    const double fy0 = (py - reach - gy0) * inv_cs, fy1 = (py + reach - gy0) * inv_cs;
+  __device__ __forceinline__ void init(float reach) {
+    marg = 1e-3f + 3e-7f * (fabsf(px) + fabsf(py) + reach);
+    const float r = reach + marg;
+    const float fy0 = (py - r) * inv_cs, fy1 = (py + r) * inv_cs;
     iy0 = 0;
     nrows = 0;
-    if (nx > 0 && ny > 0 && fy1 >= 0.0 && fy0 < (double)ny) {
-      iy0 = clampi(floor(fy0), 0, ny - 1);
-      nrows = clampi(floor(fy1), 0, ny - 1) - iy0 + 1;
+    if (nx > 0 && ny > 0 && fy1 >= 0.0f && fy0 < (float)ny) {
+      iy0 = clampf(floorf(fy0), 0, ny - 1);
+      nrows = clampf(floorf(fy1), 0, ny - 1) - iy0 + 1;
       nrows = nrows < 32 ? nrows : 32;
     }
   }
   // range of lane's row for radius `reach` (a superset of the disc's points)
-  __device__ __forceinline__ void range(double reach, int lane, int &sb, int &cnt) const {
+  __device__ __forceinline__ void range(float reach, int lane, int &sb, int &cnt) const {
     sb = 0;
     cnt = 0;
     if (lane >= nrows) return;
     const int iy = iy0 + lane;
-    const double ylo = gy0 + iy * cs, yhi = ylo + cs;
-    double dyb = 0.0;
+    const float ylo = (float)iy * cs, yhi = ylo + cs;
+    float dyb = 0.0f;
     if (py < ylo) dyb = ylo - py;
     else if (py > yhi) dyb = py - yhi;
-    if (dyb > reach) return;
-    const double half = sqrt(reach * reach - dyb * dyb) + 1e-6;
-    const double fx0 = (px - half - gx0) * inv_cs, fx1 = (px + half - gx0) * inv_cs;
-    if (fx1 < 0.0 || fx0 >= (double)nx) return;
-    const int ix0 = clampi(floor(fx0), 0, nx - 1), ix1 = clampi(floor(fx1), 0, nx - 1);
+    const float r = reach + marg;
+    if (dyb > r) return;
+    const float half = sqrtf(r * r - dyb * dyb) + marg;
+    const float fx0 = (px - half) * inv_cs, fx1 = (px + half) * inv_cs;
+    if (fx1 < 0.0f || fx0 >= (float)nx) return;
+    const int ix0 = clampf(floorf(fx0), 0, nx - 1), ix1 = clampf(floorf(fx1), 0, nx - 1);
     const int *c = cell_start + (int64_t)iy * nx;
     sb = c[ix0];
     cnt = c[ix1 + 1] - sb;
