@@ -329,10 +329,14 @@ __device__ __forceinline__ double sel_r2hi(double radius, double D) {
 // <= hint^2 + D, so the bucket window b* + 2 (+1.01 slack) stays inside
 // rho^2 - D when rho^2 (1 - 3.05 / kNB) >= hint^2 + 2D.  The floor
 // rho^2 >= 10240 D keeps the edge band beta = 2 D kNB / rho^2 <= 0.05.
-__device__ __forceinline__ double hint_radius(double hint, double radius, double D) {
-  if (!(hint > 0.0)) return radius;
-  const double r2n = fmax((hint * hint + 2.0 * D) / (1.0 - 3.05 / kNB) + 1e-3, 10240.0 * D);
-  return fmin(sqrt(r2n), radius);
+// (float arithmetic: any radius is correct here, the caller validates the
+// narrowed window against the rho it actually uses)
+__device__ __forceinline__ double hint_radius(float hint, double radius, double D) {
+  if (!(hint > 0.0f)) return radius;
+  const float Df = (float)D;
+  const float r2n = fmaxf((hint * hint + 2.0f * Df) * (1.0f / (1.0f - 3.05f / kNB)) + 1e-3f,
+                          10240.0f * Df);
+  return fmin((double)sqrtf(r2n), radius);
 }
 
 // Rank the set G[0, n_g) (bucket-sorted, counting-sort cursors in S.hc) with
@@ -342,6 +346,7 @@ template <class Src>
 __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float beta, float two_d,
                         double r2, double D, double radius, int k, const Sel &S, int lane) {
   // phase A: rank by float key; flag near ties and possibly-out-of-radius keys
+  const float r2lo = __double2float_rd(r2 - D);
   int flagged = 0;
   for (int p = lane; p < n_g; p += 32) {
     const float ap = S.ga[p];
@@ -363,7 +368,7 @@ __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float be
       rank += aq < dlo ? 1 : 0;
       amb |= aq >= dlo && aq <= dhi;
     }
-    const uint8_t f = (amb ? 1 : 0) | ((double)ap > r2 - D ? 2 : 0) | (edge ? 8 : 0);
+    const uint8_t f = (amb ? 1 : 0) | (ap > r2lo ? 2 : 0) | (edge ? 8 : 0);
     S.gf[p] = f;
     if (!(f & 3) && rank < k) S.sel_pl[rank] = S.gpl[p];
     flagged += (f & 3) != 0;
@@ -429,6 +434,10 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
                            double rho, float &bound_out) {
   if (k <= 0) return 0;
   const double r2 = radius * radius;
+  // float thresholds rounded the conservative way: Df >= D (wider bands),
+  // r2lo <= r2 - D (more keys get the exact radius test)
+  const float Df = __double2float_ru(D);
+  const float r2lo = __double2float_rd(r2 - D);
   // histogram range [0, r2hi] in key units: the whole disc, or [0, rho^2]
   // for a hint-narrowed scan (finer buckets, see hint_radius)
   float r2hi, inv_w, beta, two_d;
@@ -438,9 +447,9 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     inv_w = r2hi > 0.0f ? (float)kNB / r2hi : 0.0f;
     w = (double)r2hi / kNB;
     // edge band in bucket units: twice the key error plus float slack
-    beta = (float)(2.0 * D * (double)inv_w) + 4e-5f;
+    beta = 2.0f * Df * inv_w + 4e-5f;
     // near-tie band in float, padded by the float rounding of a - 2D
-    two_d = (float)(2.0 * D + 2.5e-7 * (double)r2hi);
+    two_d = 2.0f * Df + 2.5e-7f * r2hi;
   };
   set_range(r2 + D);
   if (!(beta < 0.125f)) return select_serial(src, k, radius, r2hi, S, lane);
@@ -482,7 +491,7 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
       }
       const float an = __shfl_down_sync(kFull, a, 1);
       const bool bad = lane < k && lane < n &&
-                       ((lane + 1 < n && an <= a + two_d) || (double)a > r2 - D);
+                       ((lane + 1 < n && an <= a + two_d) || a > r2lo);
       if (!__any_sync(kFull, bad)) {
         const int m = n < k ? n : k;
         if (lane < m) S.sel_pl[lane] = pl;
@@ -553,7 +562,7 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     }
     break;
   }
-  bound_out = total >= (uint32_t)k ? (float)(sqrt(((double)bstar + 1.0) * w + D) * (1.0 + 1e-6))
+  bound_out = total >= (uint32_t)k ? sqrtf(((float)bstar + 1.0f) * (float)w + Df) * (1.0f + 1e-6f)
                                     : 0.0f;
   if (total == 0) return 0;
   uint32_t run2 = incl - local;
@@ -746,10 +755,12 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
     float4 hint = St.obs_hint ? reinterpret_cast<const float4 *>(St.obs_hint)[g]
                               : make_float4(0.f, 0.f, 0.f, 0.f);
     float bound = 0.0f;
-    double rho_hint = 0.0;
+    // bound on this step's k-th distance: the hint plus the distance moved
+    // (float; the 1 mm slack exceeds the rounding of the grid-relative floats)
+    float rho_hint = 0.0f;
     if (hint.x > 0.0f) {
-      const double mx = (double)hint.y - (px - gx0), my = (double)hint.z - (py - gy0);
-      rho_hint = (double)hint.x + sqrt(mx * mx + my * my) + 1e-3;
+      const float mx = hint.y - (float)(px - gx0), my = hint.z - (float)(py - gy0);
+      rho_hint = hint.x + sqrtf(mx * mx + my * my) + 1e-3f;
     }
     if (cap_r > 0) {
       const double rx = px - gx0, ry = py - gy0;
