@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define DS_ABI_VERSION 2
+#define DS_ABI_VERSION 3
 #define DS_MAX_AGENTS_PER_WORLD 1024
 
 /* error codes */
@@ -135,7 +135,19 @@ typedef struct ds_tables {
    * per-world max |float - exact| of those coordinates (shared-memory scan) */
   const float *gpt_xy;
   const double *grid_eps;
+  /* grid-sorted points as 32-B records (ds_point_rec): one sector per point
+   * for the observation kernel's gather of the selected points */
+  const void *gpt_rec;
 } ds_tables;
+
+/* One road point of gpt_rec: the gpt_x / gpt_y / gpt_h / gpt_id / gpt_kind
+ * entries of the same grid-sorted index. */
+typedef struct ds_point_rec {
+  double x, y, heading;
+  int32_t id;
+  int8_t kind;
+  int8_t pad[3];
+} ds_point_rec;
 
 /* Mutable simulation state (device pointers, torch-owned). */
 typedef struct ds_state {

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # DS_LIB_PATH (dev only): an alternative build of the same library, for A/B timing
 LIB_PATH = os.environ.get("DS_LIB_PATH") or os.path.join(_HERE, "libdrivesim_b200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 OBS_F32, OBS_BF16 = 0, 1   # ds_set_obs_format element types
 
 DS_OK = 0
@@ -65,7 +65,7 @@ TABLE_PTRS = [
     "p_off", "pt_cell_start", "gpt_x", "gpt_y", "gpt_h", "gpt_kind", "gpt_id",
     "eseg_cell_start", "eseg_ax", "eseg_ay", "eseg_bx", "eseg_by",
     "aseg_cell_start", "aseg_ax", "aseg_ay", "aseg_bx", "aseg_by", "aseg_id", "aseg_edge",
-    "s_off", "gpt_xy", "grid_eps",
+    "s_off", "gpt_xy", "grid_eps", "gpt_rec",
 ]
 
 

@@ -180,8 +180,7 @@ struct PartnerSrc {
 // |pr - (px - x0)| measured per agent: see the bound D in the kernel.
 struct RoadSrcShared {
   const float2 *pts;                 // shared, world-relative index
-  const double *__restrict__ gx, *__restrict__ gy;
-  const int *__restrict__ gid;
+  const ds_point_rec *__restrict__ rec;
   int p0;
   float prx, pry;
   double px, py;
@@ -212,8 +211,9 @@ struct RoadSrcShared {
     }
   }
   __device__ __forceinline__ double exact(int pl, int &id) const {
-    id = gid[p0 + pl];
-    return hypot(gx[p0 + pl] - px, gy[p0 + pl] - py);
+    const ds_point_rec &q = rec[p0 + pl];
+    id = q.id;
+    return hypot(q.x - px, q.y - py);
   }
 };
 
@@ -772,7 +772,8 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
         const double E = eps_p + fmax(fabs((double)prx - rx), fabs((double)pry - ry)) + K.key_e;
         const double D = 4.0 * (radius + 1.0) * E + 2.0 * E * E + D_fp64;
         const double rho = hint_radius(rho_hint, radius, D);
-        RoadSrcShared rsrc{pts, T.gpt_x, T.gpt_y, T.gpt_id, (int)p0, prx, pry, px, py, &geo};
+        RoadSrcShared rsrc{pts, static_cast<const ds_point_rec *>(T.gpt_rec), (int)p0, prx, pry, px,
+                           py, &geo};
         rsrc.cover(rho < radius ? rho : reach, lane);
         mr = select_topk<false>(rsrc, cap_r, radius, D, S, lane, rho, bound);
       } else {
@@ -792,15 +793,32 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
       float *slot = rstage + 11 * m;
       if (m < mr) {
         const int s = S.sel_pl[m] + sel_off;
-        const double dx = T.gpt_x[s] - px, dy = T.gpt_y[s] - py;
-        const int kind = T.gpt_kind[s];
+        double qx, qy, qh;
+        int kind, qid;
+        if (SharedPts) {
+          // one 32-B record (ds_point_rec): two 16-B loads of one sector
+          const double2 *r2 = reinterpret_cast<const double2 *>(T.gpt_rec) + 2 * (int64_t)s;
+          const double2 a = r2[0], b = r2[1];
+          qx = a.x;
+          qy = a.y;
+          qh = b.x;
+          qid = __double2loint(b.y);
+          kind = (int)(signed char)(__double2hiint(b.y) & 0xff);
+        } else {
+          qx = T.gpt_x[s];
+          qy = T.gpt_y[s];
+          qh = T.gpt_h[s];
+          kind = T.gpt_kind[s];
+          qid = T.gpt_id[s];
+        }
+        const double dx = qx - px, dy = qy - py;
         slot[0] = (float)(dx * ch + dy * sh);
         slot[1] = (float)(dy * ch - dx * sh);
-        slot[2] = (float)wrap(T.gpt_h[s] - h);
+        slot[2] = (float)wrap(qh - h);
 #pragma unroll
         for (int q = 0; q < 7; ++q) slot[3 + q] = q == kind ? 1.0f : 0.0f;
         slot[10] = 1.0f;
-        if (sel_idx) sel_idx[orow * sel_w + cap_a + m] = T.gpt_id[s];
+        if (sel_idx) sel_idx[orow * sel_w + cap_a + m] = qid;
       } else {
 #pragma unroll
         for (int q = 0; q < 11; ++q) slot[q] = 0.0f;
@@ -838,7 +856,7 @@ void obs_plan(ds_handle *h, int max_optin) {
     h->obs_smem = lidar_smem_bytes(h->tab.max_agents, h->obs_width);
     return;
   }
-  const bool can = h->tab.gpt_xy && h->tab.grid_eps;
+  const bool can = h->tab.gpt_xy && h->tab.grid_eps && h->tab.gpt_rec;
   const size_t sh = obs_smem_bytes_shared(h->cfg, h->tab.max_agents, h->tab.max_points, kWarpsShared);
   const size_t sh_small =
       obs_smem_bytes_shared(h->cfg, h->tab.max_agents, h->tab.max_points, kWarpsSharedSmall);

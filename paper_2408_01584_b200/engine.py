@@ -290,6 +290,14 @@ class SimBatch:
                      "aseg_cell_start", "aseg_ax", "aseg_ay", "aseg_bx", "aseg_by", "aseg_id",
                      "aseg_edge", "gpt_xy", "grid_eps"):
             t[name] = _dev(getattr(lay, name), dev)
+        # 32-B point records (ds_point_rec) for the observation slot gather
+        rec = np.zeros(max(len(lay.gpt_x), 1), dtype=np.dtype(
+            [("x", "<f8"), ("y", "<f8"), ("h", "<f8"), ("id", "<i4"), ("kind", "i1"),
+             ("pad", "i1", (3,))]))
+        if len(lay.gpt_x):
+            rec["x"], rec["y"], rec["h"] = lay.gpt_x, lay.gpt_y, lay.gpt_h
+            rec["id"], rec["kind"] = lay.gpt_id, lay.gpt_kind
+        t["gpt_rec"] = torch.from_numpy(rec.view(np.uint8)).to(dev)
         t["p_off"] = _dev(pw.p_off, dev)
         t["s_off"] = _dev(pw.s_off, dev)
         self._t_tensors = t
