@@ -19,6 +19,9 @@ namespace ds {
 struct StepShared {
   double *x, *y, *c, *s, *hl, *hw, *cr;
   uint8_t *elig;
+  // circumcircle prefilter: float position relative to the world's grid
+  // origin, circumradius padded by the float rounding bound (> 0: eligible)
+  float4 *pre;
 };
 
 __device__ __forceinline__ StepShared carve_step(void *base, int amax) {
@@ -32,11 +35,13 @@ __device__ __forceinline__ StepShared carve_step(void *base, int amax) {
   sh.hw = d + 5 * amax;
   sh.cr = d + 6 * amax;
   sh.elig = reinterpret_cast<uint8_t *>(d + 7 * amax);
+  sh.pre = reinterpret_cast<float4 *>(
+      (reinterpret_cast<uintptr_t>(sh.elig + amax) + 15) & ~uintptr_t(15));
   return sh;
 }
 
 size_t step_smem_bytes(int max_agents) {
-  return (size_t)max_agents * (7 * sizeof(double) + 1) + 16;
+  return (size_t)max_agents * (7 * sizeof(double) + 1) + 16 + (size_t)max_agents * sizeof(float4);
 }
 
 // SAT over the 4 box axes, _fastpath.sat_pairs (fp:29-53); (i, j) with i < j.
@@ -142,7 +147,10 @@ __device__ __forceinline__ void reset_agent(const ds_tables &T, const ds_state &
   S.flags[g] = present ? DS_F_PRESENT : 0;
 }
 
-__global__ void __launch_bounds__(1024) step_kernel(ds_tables T, ds_config C, ds_state S,
+// MAXT: the launch's thread bound (worlds of <= 256 agents get the 256
+// variant: up to 255 registers, no spills of the FP64 state)
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) step_kernel(ds_tables T, ds_config C, ds_state S,
                                                     ds_step_args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int w = blockIdx.x;
@@ -279,17 +287,24 @@ __global__ void __launch_bounds__(1024) step_kernel(ds_tables T, ds_config C, ds
     const bool elig = (f & DS_F_PRESENT) && !(f & DS_F_REMOVED) &&
                       ((ctrl && !(f & DS_F_DONE)) || T.rep_valid[rn]);
     sh.elig[tid] = elig;
+    // |fx - (x - x0)| <= 2^-24 |x - x0|: pad the radius by 2.4e-7 (|fx| + |fy|)
+    // + 1 mm, so that float distances > the padded sum prove disjoint circles
+    const float fx = (float)(x - T.grid_x0[w]), fy = (float)(y - T.grid_y0[w]);
+    const float pr = (float)T.circumradius[g] * (1.0f + 1e-6f) + 1e-3f +
+                     2.4e-7f * (fabsf(fx) + fabsf(fy));
+    sh.pre[tid] = make_float4(fx, fy, pr, elig ? 1.0f : 0.0f);
   }
   __syncthreads();
 
   bool collided = false, offroad = false;
   if (act_here && sh.elig[tid]) {
-    const double xi = sh.x[tid], yi = sh.y[tid], cri = sh.cr[tid];
+    const float4 pi = sh.pre[tid];
     for (int j = 0; j < A; ++j) {
-      if (j == tid || !sh.elig[j]) continue;
       // boxes lie inside their circumcircles: disjoint circles cannot collide
-      const double dx = sh.x[j] - xi, dy = sh.y[j] - yi, rr = cri + sh.cr[j];
-      if (dx * dx + dy * dy > rr * rr * (1.0 + 1e-9) + 1e-9) continue;
+      // (float superset test on padded radii; SAT below decides exactly)
+      const float4 pj = sh.pre[j];
+      const float dx = pj.x - pi.x, dy = pj.y - pi.y, rr = pi.z + pj.z;
+      if (pj.w == 0.0f || fmaf(dx, dx, dy * dy) > rr * rr * (1.0f + 1e-5f) || j == tid) continue;
       if (j > tid ? sat_hit(sh, tid, j) : sat_hit(sh, j, tid)) {
         collided = true;
         break;
@@ -392,12 +407,20 @@ __global__ void __launch_bounds__(1024) reset_kernel(ds_tables T, ds_state S, co
 }
 
 cudaError_t configure_step_kernels(int max_dynamic_smem) {
-  return cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(step_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       max_dynamic_smem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(step_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               max_dynamic_smem);
 }
 
 cudaError_t launch_step(const ds_handle *h, const ds_step_args *a, cudaStream_t s) {
-  step_kernel<<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg, h->st, *a);
+  if (h->step_threads <= 256)
+    step_kernel<256><<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg, h->st,
+                                                                           *a);
+  else
+    step_kernel<1024><<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg, h->st,
+                                                                            *a);
   return cudaGetLastError();
 }
 
