@@ -138,6 +138,9 @@ typedef struct ds_tables {
   /* grid-sorted points as 32-B records (ds_point_rec): one sector per point
    * for the observation kernel's gather of the selected points */
   const void *gpt_rec;
+  /* road-edge segments of eseg_* as float (ax, ay, bx, by) relative to the
+   * world's grid origin, 16 B per entry: the off-road AABB prefilter */
+  const float *eseg_rel;
 } ds_tables;
 
 /* One road point of gpt_rec: the gpt_x / gpt_y / gpt_h / gpt_id / gpt_kind

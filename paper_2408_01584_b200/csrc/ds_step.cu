@@ -19,6 +19,7 @@ namespace ds {
 struct StepShared {
   double *x, *y, *c, *s, *hl, *hw, *cr;
   uint8_t *elig;
+  uint8_t *hit;    // agent-agent collision flags (each pair tested once)
   // circumcircle prefilter: float position relative to the world's grid
   // origin, circumradius padded by the float rounding bound (> 0: eligible)
   float4 *pre;
@@ -35,13 +36,14 @@ __device__ __forceinline__ StepShared carve_step(void *base, int amax) {
   sh.hw = d + 5 * amax;
   sh.cr = d + 6 * amax;
   sh.elig = reinterpret_cast<uint8_t *>(d + 7 * amax);
+  sh.hit = sh.elig + amax;
   sh.pre = reinterpret_cast<float4 *>(
-      (reinterpret_cast<uintptr_t>(sh.elig + amax) + 15) & ~uintptr_t(15));
+      (reinterpret_cast<uintptr_t>(sh.hit + amax) + 15) & ~uintptr_t(15));
   return sh;
 }
 
 size_t step_smem_bytes(int max_agents) {
-  return (size_t)max_agents * (7 * sizeof(double) + 1) + 16 + (size_t)max_agents * sizeof(float4);
+  return (size_t)max_agents * (7 * sizeof(double) + 2) + 16 + (size_t)max_agents * sizeof(float4);
 }
 
 // SAT over the 4 box axes, _fastpath.sat_pairs (fp:29-53); (i, j) with i < j.
@@ -113,6 +115,12 @@ __device__ bool offroad_query(const ds_tables &T, const ds_config &C, int w, dou
   // only has to produce a superset, the slab test below decides.
   const double rx = hl * fabs(ck) + hw * fabs(sk) + 0.011;
   const double ry = hl * fabs(sk) + hw * fabs(ck) + 0.011;
+  // float prefilter on the grid-relative copies (16 B per segment): widened
+  // by a bound on its rounding, it only skips segments the FP64 test skips
+  const float fcx = (float)(cx - x0), fcy = (float)(cy - y0);
+  const float fm = 1e-3f + 2.4e-7f * (fabsf(fcx) + fabsf(fcy) + (float)(rx + ry));
+  const float frx = (float)rx + fm, fry = (float)ry + fm;
+  const float4 *erel = reinterpret_cast<const float4 *>(T.eseg_rel);
   const double gx0 = (cx - rx - x0) / cs, gx1 = (cx + rx - x0) / cs;
   const double gy0 = (cy - ry - y0) / cs, gy1 = (cy + ry - y0) / cs;
   if (gx1 < 0.0 || gy1 < 0.0 || gx0 >= (double)nx || gy0 >= (double)ny) return false;
@@ -123,6 +131,10 @@ __device__ bool offroad_query(const ds_tables &T, const ds_config &C, int w, dou
       const int64_t cell = cbase + (int64_t)iy * nx + ix;
       const int b = T.eseg_cell_start[cell], e = T.eseg_cell_start[cell + 1];
       for (int k = b; k < e; ++k) {
+        const float4 q = erel[k];
+        if (fmaxf(q.x, q.z) < fcx - frx || fminf(q.x, q.z) > fcx + frx ||
+            fmaxf(q.y, q.w) < fcy - fry || fminf(q.y, q.w) > fcy + fry)
+          continue;
         const double ax = T.eseg_ax[k], ay = T.eseg_ay[k], bx = T.eseg_bx[k], by = T.eseg_by[k];
         // segment AABB vs box AABB (with slack): a superset prefilter
         if (fmax(ax, bx) < cx - rx || fmin(ax, bx) > cx + rx || fmax(ay, by) < cy - ry ||
@@ -293,23 +305,36 @@ __global__ void __launch_bounds__(MAXT) step_kernel(ds_tables T, ds_config C, ds
     const float pr = (float)T.circumradius[g] * (1.0f + 1e-6f) + 1e-3f +
                      2.4e-7f * (fabsf(fx) + fabsf(fy));
     sh.pre[tid] = make_float4(fx, fy, pr, elig ? 1.0f : 0.0f);
+    sh.hit[tid] = 0;
   }
   __syncthreads();
 
   bool collided = false, offroad = false;
   if (act_here && sh.elig[tid]) {
+    // every unordered pair once: agent i tests i + 1 .. i + A/2 (mod A) and
+    // flags both ends (SAT always runs on (min, max), so the result is the
+    // one either end would compute)
     const float4 pi = sh.pre[tid];
-    for (int j = 0; j < A; ++j) {
+    const int half = A >> 1;
+    bool hit_any = false;
+    for (int d = 1; d <= half; ++d) {
+      int j = tid + d;
+      if (j >= A) j -= A;
       // boxes lie inside their circumcircles: disjoint circles cannot collide
       // (float superset test on padded radii; SAT below decides exactly)
       const float4 pj = sh.pre[j];
       const float dx = pj.x - pi.x, dy = pj.y - pi.y, rr = pi.z + pj.z;
-      if (pj.w == 0.0f || fmaf(dx, dx, dy * dy) > rr * rr * (1.0f + 1e-5f) || j == tid) continue;
+      if (pj.w == 0.0f || fmaf(dx, dx, dy * dy) > rr * rr * (1.0f + 1e-5f)) continue;
       if (j > tid ? sat_hit(sh, tid, j) : sat_hit(sh, j, tid)) {
-        collided = true;
-        break;
+        hit_any = true;
+        sh.hit[j] = 1;
       }
     }
+    if (hit_any) sh.hit[tid] = 1;
+  }
+  __syncthreads();
+  if (act_here && sh.elig[tid]) {
+    collided = sh.hit[tid] != 0;
     if (!(sf & DS_SF_PEDESTRIAN))
       offroad = offroad_query(T, C, w, sh.x[tid], sh.y[tid], sh.c[tid], sh.s[tid], sh.hl[tid],
                               sh.hw[tid]);

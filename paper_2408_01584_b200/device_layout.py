@@ -44,6 +44,7 @@ class DeviceLayout:
     eseg_ay: np.ndarray
     eseg_bx: np.ndarray
     eseg_by: np.ndarray
+    eseg_rel: np.ndarray      # f32 [E, 4] (ax, ay, bx, by) - grid origin (off-road prefilter)
     aseg_cell_start: np.ndarray
     aseg_ax: np.ndarray
     aseg_ay: np.ndarray
@@ -144,6 +145,9 @@ def build_layout(pw: PackedWorlds, cell: float = 8.0, all_segments: bool = True)
     as_, aorder = _bin_segments(pw, np.full(len(world_of_seg), bool(all_segments)), world_of_seg,
                                 x0, y0, nx, ny, cell_base, n_cells_total, cell)
     seg_local = np.arange(len(world_of_seg)) - np.repeat(pw.s_off[:-1], S)
+    ew = world_of_seg[eorder]
+    erel = np.stack([pw.seg_ax[eorder] - x0[ew], pw.seg_ay[eorder] - y0[ew],
+                     pw.seg_bx[eorder] - x0[ew], pw.seg_by[eorder] - y0[ew]], -1).astype(np.float32)
     # float2 coordinates relative to the world origin for the shared-memory scan,
     # with the exact per-world rounding bound used by the key error analysis
     ws = world_of_pt[order] if len(order) else np.zeros(0, np.int64)
@@ -163,6 +167,7 @@ def build_layout(pw: PackedWorlds, cell: float = 8.0, all_segments: bool = True)
         gpt_id=local[order].astype(np.int32),
         eseg_cell_start=per_world_ptr(es), eseg_ax=pw.seg_ax[eorder], eseg_ay=pw.seg_ay[eorder],
         eseg_bx=pw.seg_bx[eorder], eseg_by=pw.seg_by[eorder],
+        eseg_rel=np.ascontiguousarray(erel.reshape(-1, 4)),
         aseg_cell_start=per_world_ptr(as_), aseg_ax=pw.seg_ax[aorder], aseg_ay=pw.seg_ay[aorder],
         aseg_bx=pw.seg_bx[aorder], aseg_by=pw.seg_by[aorder],
         aseg_id=seg_local[aorder].astype(np.int32), aseg_edge=edge[aorder].astype(np.uint8),

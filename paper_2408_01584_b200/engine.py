@@ -288,7 +288,7 @@ class SimBatch:
                      "pt_cell_start", "gpt_x", "gpt_y", "gpt_h", "gpt_kind", "gpt_id",
                      "eseg_cell_start", "eseg_ax", "eseg_ay", "eseg_bx", "eseg_by",
                      "aseg_cell_start", "aseg_ax", "aseg_ay", "aseg_bx", "aseg_by", "aseg_id",
-                     "aseg_edge", "gpt_xy", "grid_eps"):
+                     "aseg_edge", "gpt_xy", "grid_eps", "eseg_rel"):
             t[name] = _dev(getattr(lay, name), dev)
         # 32-B point records (ds_point_rec) for the observation slot gather
         rec = np.zeros(max(len(lay.gpt_x), 1), dtype=np.dtype(
