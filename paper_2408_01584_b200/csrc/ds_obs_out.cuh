@@ -41,19 +41,23 @@ __device__ __forceinline__ void write_row(const ObsOut &o, int64_t orow, const f
     const int nvec = vec && width > head ? (width - head) >> 2 : 0;
     const int tail0 = head < width ? head + 4 * nvec : width;
     if (lane < head && lane < width) out[lane] = scaled(row, scale, lane);
-    const float4 *rv = reinterpret_cast<const float4 *>(row + head);
-    float4 *ov = reinterpret_cast<float4 *>(out + head);
+    const float4 *rv = reinterpret_cast<const float4 *>(row + head) + lane;
+    float4 *ov = reinterpret_cast<float4 *>(out + head) + lane;
+    const int nv = nvec > lane ? (nvec - lane + 31) >> 5 : 0;   // this lane's vectors
+    if (!scale) {
+#pragma unroll 4
+      for (int q = 0; q < nv; ++q) ov[32 * q] = rv[32 * q];
+    } else {
 #pragma unroll 1
-    for (int v = lane; v < nvec; v += 32) {
-      float4 x = rv[v];
-      if (scale) {
-        const float *sc = scale + head + 4 * v;
+      for (int q = 0; q < nv; ++q) {
+        float4 x = rv[32 * q];
+        const float *sc = scale + head + 4 * (lane + 32 * q);
         x.x /= sc[0];
         x.y /= sc[1];
         x.z /= sc[2];
         x.w /= sc[3];
+        ov[32 * q] = x;
       }
-      ov[v] = x;
     }
 #pragma unroll 1
     for (int c = tail0 + lane; c < width; c += 32) out[c] = scaled(row, scale, c);
