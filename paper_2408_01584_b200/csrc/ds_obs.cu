@@ -469,34 +469,27 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     if (n == 0) return 0;
     __syncwarp();
     if (n <= 32) {
-      // one candidate per lane: warp bitonic sort by (key, payload); keys more
-      // than 2D apart order exactly like the distances, so the sorted order is
-      // the reference's unless a near tie or a possibly-out-of-radius key sits
-      // inside the first k (then the exact ranking below decides)
-      float a = lane < n ? S.ga[lane] : INFINITY;
-      int pl = lane < n ? S.gpl[lane] : 0x7fffffff;
-#pragma unroll
-      for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          const float oa = __shfl_xor_sync(kFull, a, stride);
-          const int opl = __shfl_xor_sync(kFull, pl, stride);
-          const bool o_less = oa < a || (oa == a && opl < pl);
-          const bool want_min = ((lane & stride) == 0) == ((lane & size) == 0 || size == 32);
-          if (want_min == o_less) {
-            a = oa;
-            pl = opl;
-          }
-        }
+      // one candidate per lane, ranked by counting (key, payload) order over
+      // the n broadcast keys; keys more than 2D apart order exactly like the
+      // distances, so the ranks are the reference's unless a near tie or a
+      // possibly-out-of-radius key sits inside the first k (then the exact
+      // ranking below decides)
+      const float a = lane < n ? S.ga[lane] : INFINITY;
+      const int pl = lane < n ? S.gpl[lane] : 0x7fffffff;
+      int rank = 0;
+      bool amb = false;
+#pragma unroll 4
+      for (int j = 0; j < n; ++j) {
+        const float aj = __shfl_sync(kFull, a, j);
+        const int plj = __shfl_sync(kFull, pl, j);
+        rank += (aj < a || (aj == a && plj < pl)) ? 1 : 0;
+        amb |= j != lane && fabsf(aj - a) <= two_d;
       }
-      const float an = __shfl_down_sync(kFull, a, 1);
-      const bool bad = lane < k && lane < n &&
-                       ((lane + 1 < n && an <= a + two_d) || a > r2lo);
+      const bool bad = lane < n && rank < k && (amb || a > r2lo);
       if (!__any_sync(kFull, bad)) {
-        const int m = n < k ? n : k;
-        if (lane < m) S.sel_pl[lane] = pl;
+        if (lane < n && rank < k) S.sel_pl[rank] = pl;
         __syncwarp();
-        return m;
+        return n < k ? n : k;
       }
     }
     if (n <= S.gcap && n <= 0xffff) {
@@ -515,8 +508,11 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
   uint32_t total, n_g, incl, local;
   uint32_t cnt[kPer];
   int bstar, bmax, nbuf;
+  static_assert(kPer == 8, "the histogram is read / written as two uint4 per lane");
+  uint4 *const hc4 = reinterpret_cast<uint4 *>(S.hc);
   while (true) {
-    for (int b = lane; b < kNB; b += 32) S.hc[b] = 0u;
+    hc4[lane] = make_uint4(0u, 0u, 0u, 0u);
+    hc4[lane + 32] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
     nbuf = 0;
     src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
@@ -530,12 +526,14 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
       nbuf += __popc(bal);
     });
     __syncwarp();
+    {
+      const uint4 c0 = hc4[2 * lane], c1 = hc4[2 * lane + 1];
+      cnt[0] = c0.x; cnt[1] = c0.y; cnt[2] = c0.z; cnt[3] = c0.w;
+      cnt[4] = c1.x; cnt[5] = c1.y; cnt[6] = c1.z; cnt[7] = c1.w;
+    }
     local = 0;
 #pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      cnt[q] = S.hc[lane * kPer + q];
-      local += cnt[q];
-    }
+    for (int q = 0; q < kPer; ++q) local += cnt[q];
     incl = local;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -567,13 +565,16 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
   if (total == 0) return 0;
   uint32_t run2 = incl - local;
   n_g = 0;
+  uint32_t hv[kPer];
 #pragma unroll
   for (int q = 0; q < kPer; ++q) {
     const int b = lane * kPer + q;
-    S.hc[b] = (run2 << 16) | cnt[q];
+    hv[q] = (run2 << 16) | cnt[q];
     run2 += cnt[q];
     if (b == bmax) n_g = run2;
   }
+  hc4[2 * lane] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+  hc4[2 * lane + 1] = make_uint4(hv[4], hv[5], hv[6], hv[7]);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) n_g = max(n_g, __shfl_xor_sync(kFull, n_g, off));
   __syncwarp();
