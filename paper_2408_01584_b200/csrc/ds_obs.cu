@@ -360,14 +360,15 @@ __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float be
     const int start = (int)(hlo >> 16) - (int)(hlo & 0xffffu);
     const int end = (int)(hhi >> 16);
     const float dlo = ap - two_d, dhi = ap + two_d;
-    int rank = start;
-    bool amb = false;
+    // branch-free window scan; p itself lies in the window (never below dlo,
+    // always inside the band: one band count is its own)
+    int rank = start, nband = 0;
     for (int q = start; q < end; ++q) {
-      if (q == p) continue;
       const float aq = S.ga[q];
       rank += aq < dlo ? 1 : 0;
-      amb |= aq >= dlo && aq <= dhi;
+      nband += (aq >= dlo && aq <= dhi) ? 1 : 0;
     }
+    const bool amb = nband > 1;
     const uint8_t f = (amb ? 1 : 0) | (ap > r2lo ? 2 : 0) | (edge ? 8 : 0);
     S.gf[p] = f;
     if (!(f & 3) && rank < k) S.sel_pl[rank] = S.gpl[p];
