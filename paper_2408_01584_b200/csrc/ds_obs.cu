@@ -158,13 +158,10 @@ struct PartnerSrc {
     #pragma unroll 1
     for (int f0 = 0; f0 < n; f0 += 32) {
       const int f = f0 + lane;
-      bool ok = f < n && f != self && vis[f];
-      float a = 0.0f;
-      if (ok) {
-        const double dx = x[f] - px, dy = y[f] - py;
-        a = (float)fma(dx, dx, dy * dy);
-        ok = a <= r2hi;
-      }
+      const int fs = f < n ? f : n - 1;   // branch-free: every lane computes a key
+      const double dx = x[fs] - px, dy = y[fs] - py;
+      const float a = (float)fma(dx, dx, dy * dy);
+      const bool ok = f < n && f != self && vis[fs] && a <= r2hi;
       fn(ok, a, f);
     }
   }
@@ -198,15 +195,13 @@ struct RoadSrcShared {
   __device__ __forceinline__ void visit(float r2hi, int lane, F &&fn) const {
     #pragma unroll 1
     for (int f0 = 0; f0 < rows.total; f0 += 32) {
-      const int s = rows.map(f0, lane);
-      bool ok = f0 + lane < rows.total;
-      float a = 0.0f;
-      if (ok) {
-        const float2 p = pts[s];
-        const float dx = p.x - prx, dy = p.y - pry;
-        a = fmaf(dx, dx, dy * dy);
-        ok = a <= r2hi;
-      }
+      const bool in = f0 + lane < rows.total;
+      const int sm = rows.map(f0, lane);
+      const int s = in ? sm : 0;   // branch-free: lanes past the end read point 0
+      const float2 p = pts[s];
+      const float dx = p.x - prx, dy = p.y - pry;
+      const float a = fmaf(dx, dx, dy * dy);
+      const bool ok = in && a <= r2hi;
       fn(ok, a, s);
     }
   }
