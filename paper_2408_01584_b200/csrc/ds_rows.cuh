@@ -69,7 +69,7 @@ struct RowGeo {
 // number of row ends inside (f0, f0 + o]: one OR-reduction of end offsets
 // and a popcount (ends are distinct because empty rows were dropped).
 struct FlatRows {
-  int sb, cnt, pe, nr, total, src;
+  int sb, cnt, pe, nr, total, src, base;
   __device__ __forceinline__ void build(int sb_in, int cnt_in, int lane) {
     const unsigned bal = __ballot_sync(kFullMask, cnt_in > 0);
     nr = __popc(bal);
@@ -85,6 +85,7 @@ struct FlatRows {
       if (lane >= off) pe += up;
     }
     total = __shfl_sync(kFullMask, pe, 31);
+    base = sb - (pe - cnt);   // element index of flattened position f in this row: base + f
   }
   // point index of flattened candidate f0 + lane (valid when f0 + lane < total)
   __device__ __forceinline__ int map(int f0, int lane) const {
@@ -93,10 +94,7 @@ struct FlatRows {
     const int off = pe - f0;
     const unsigned E = __reduce_or_sync(kFullMask, (live && off > 0 && off < 32) ? (1u << off) : 0u);
     const int r = (r0 + __popc(E & ((2u << lane) - 1u))) & 31;
-    const int rs = __shfl_sync(kFullMask, sb, r);
-    const int rpe = __shfl_sync(kFullMask, pe, r);
-    const int rc = __shfl_sync(kFullMask, cnt, r);
-    return rs + (f0 + lane - (rpe - rc));
+    return __shfl_sync(kFullMask, base, r) + f0 + lane;
   }
   // as map(), also returning the original lane that owned the range
   __device__ __forceinline__ int map_owner(int f0, int lane, int &owner) const {
@@ -105,11 +103,8 @@ struct FlatRows {
     const int off = pe - f0;
     const unsigned E = __reduce_or_sync(kFullMask, (live && off > 0 && off < 32) ? (1u << off) : 0u);
     const int r = (r0 + __popc(E & ((2u << lane) - 1u))) & 31;
-    const int rs = __shfl_sync(kFullMask, sb, r);
-    const int rpe = __shfl_sync(kFullMask, pe, r);
-    const int rc = __shfl_sync(kFullMask, cnt, r);
     owner = __shfl_sync(kFullMask, src, r);
-    return rs + (f0 + lane - (rpe - rc));
+    return __shfl_sync(kFullMask, base, r) + f0 + lane;
   }
 };
 
