@@ -470,17 +470,22 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
       // distances, so the ranks are the reference's unless a near tie or a
       // possibly-out-of-radius key sits inside the first k (then the exact
       // ranking below decides)
+      // (non-negative float keys order like their bit patterns: one 64-bit
+      // compare of (key bits, payload) per broadcast; near ties are found
+      // afterwards between sorted neighbours, staged in the idle pass-1 buffer)
       const float a = lane < n ? S.ga[lane] : INFINITY;
       const int pl = lane < n ? S.gpl[lane] : 0x7fffffff;
+      const unsigned long long key =
+          ((unsigned long long)__float_as_uint(a) << 32) | (unsigned long long)(unsigned)pl;
       int rank = 0;
-      bool amb = false;
 #pragma unroll 4
-      for (int j = 0; j < n; ++j) {
-        const float aj = __shfl_sync(kFull, a, j);
-        const int plj = __shfl_sync(kFull, pl, j);
-        rank += (aj < a || (aj == a && plj < pl)) ? 1 : 0;
-        amb |= j != lane && fabsf(aj - a) <= two_d;
-      }
+      for (int j = 0; j < n; ++j) rank += __shfl_sync(kFull, key, j) < key ? 1 : 0;
+      float *const srt = S.ca;
+      if (lane < n) srt[rank] = a;
+      __syncwarp();
+      bool amb = false;
+      if (lane < n)
+        amb = (rank + 1 < n && srt[rank + 1] - a <= two_d) || (rank > 0 && a - srt[rank - 1] <= two_d);
       const bool bad = lane < n && rank < k && (amb || a > r2lo);
       if (!__any_sync(kFull, bad)) {
         if (lane < n && rank < k) S.sel_pl[rank] = pl;
