@@ -565,20 +565,19 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
                                     : 0.0f;
   if (total == 0) return 0;
   uint32_t run2 = incl - local;
-  n_g = 0;
   uint32_t hv[kPer];
 #pragma unroll
   for (int q = 0; q < kPer; ++q) {
-    const int b = lane * kPer + q;
     hv[q] = (run2 << 16) | cnt[q];
     run2 += cnt[q];
-    if (b == bmax) n_g = run2;
   }
   hc4[2 * lane] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
   hc4[2 * lane + 1] = make_uint4(hv[4], hv[5], hv[6], hv[7]);
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) n_g = max(n_g, __shfl_xor_sync(kFull, n_g, off));
   __syncwarp();
+  {
+    const uint32_t hb = S.hc[bmax];   // (start << 16) | count of the last kept bucket
+    n_g = (hb >> 16) + (hb & 0xffffu);
+  }
   if (n_g > (uint32_t)S.gcap || total > 0xffffu) {
     src.restrict_to(radius + 1e-6, lane);
     return select_serial(src, k, radius, r2hi, S, lane);
