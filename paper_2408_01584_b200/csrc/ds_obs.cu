@@ -117,16 +117,22 @@ size_t obs_smem_bytes_global(const ds_config &cfg, int max_agents) {
   return agents_bytes(max_agents) + warp_layout(cfg, true).total * kWarpsGlobal;
 }
 
+// Per-warp selection scratch: one base pointer plus the layout's offsets
+// (compile-time for the default caps, so every array is base + immediate).
 struct Sel {
-  uint32_t *hc;
-  float *ca;
-  uint16_t *cp;
-  float *ga;
-  double *ge;
-  int *gid, *gpl;
-  uint8_t *gb, *gf;
-  int *sel_pl;
+  unsigned char *wb;
+  WarpLayout L;
   int gcap, ccap;
+  __device__ __forceinline__ uint32_t *hc() const { return reinterpret_cast<uint32_t *>(wb + L.hc); }
+  __device__ __forceinline__ float *ca() const { return reinterpret_cast<float *>(wb + L.ca); }
+  __device__ __forceinline__ uint16_t *cp() const { return reinterpret_cast<uint16_t *>(wb + L.cp); }
+  __device__ __forceinline__ float *ga() const { return reinterpret_cast<float *>(wb + L.ga); }
+  __device__ __forceinline__ double *ge() const { return reinterpret_cast<double *>(wb + L.ge); }
+  __device__ __forceinline__ int *gid() const { return reinterpret_cast<int *>(wb + L.gid); }
+  __device__ __forceinline__ int *gpl() const { return reinterpret_cast<int *>(wb + L.gpl); }
+  __device__ __forceinline__ uint8_t *gb() const { return wb + L.gb; }
+  __device__ __forceinline__ uint8_t *gf() const { return wb + L.gf; }
+  __device__ __forceinline__ int *sel_pl() const { return reinterpret_cast<int *>(wb + L.sel_pl); }
 };
 
 __device__ __forceinline__ bool key_less(double da, int ia, double db, int ib) {
@@ -273,22 +279,22 @@ __device__ int select_serial(const Src &src, int k, double radius, float r2hi, c
         bool take = true;
         if (cnt < k) {
           m = cnt++;
-        } else if (key_less(ej, idj, S.ge[k - 1], S.gid[k - 1])) {
+        } else if (key_less(ej, idj, S.ge()[k - 1], S.gid()[k - 1])) {
           m = k - 1;
         } else {
           take = false;
           m = 0;
         }
         if (take) {
-          while (m > 0 && key_less(ej, idj, S.ge[m - 1], S.gid[m - 1])) {
-            S.ge[m] = S.ge[m - 1];
-            S.gid[m] = S.gid[m - 1];
-            S.gpl[m] = S.gpl[m - 1];
+          while (m > 0 && key_less(ej, idj, S.ge()[m - 1], S.gid()[m - 1])) {
+            S.ge()[m] = S.ge()[m - 1];
+            S.gid()[m] = S.gid()[m - 1];
+            S.gpl()[m] = S.gpl()[m - 1];
             --m;
           }
-          S.ge[m] = ej;
-          S.gid[m] = idj;
-          S.gpl[m] = plj;
+          S.ge()[m] = ej;
+          S.gid()[m] = idj;
+          S.gpl()[m] = plj;
         }
       }
       __syncwarp();
@@ -296,14 +302,14 @@ __device__ int select_serial(const Src &src, int k, double radius, float r2hi, c
   });
   cnt = __shfl_sync(kFull, cnt, 0);
   for (int m = lane; m < cnt; m += 32) {
-    S.sel_pl[m] = S.gpl[m];
+    S.sel_pl()[m] = S.gpl()[m];
   }
   __syncwarp();
   return cnt;
 }
 
 // Exact ascending top-min(n_valid, k) by (distance, id) given candidate keys
-// with |a - d^2| <= D.  Payloads land in S.sel_pl[0..m).  Warp-collective.
+// with |a - d^2| <= D.  Payloads land in S.sel_pl()[0..m).  Warp-collective.
 //  * rho: the radius the source currently covers (< radius when the caller
 //    narrowed it with a search hint, see hint_radius).  A narrowed pass 1 is
 //    used only if every bucket the selection touches provably lies inside
@@ -334,9 +340,9 @@ __device__ __forceinline__ double hint_radius(float hint, double radius, double 
   return fmin((double)sqrtf(r2n), radius);
 }
 
-// Rank the set G[0, n_g) (bucket-sorted, counting-sort cursors in S.hc) with
+// Rank the set G[0, n_g) (bucket-sorted, counting-sort cursors in S.hc()) with
 // the float keys; near ties and possibly-out-of-radius keys get the exact
-// (distance, id) treatment.  Returns min(#valid, k); payloads in S.sel_pl.
+// (distance, id) treatment.  Returns min(#valid, k); payloads in S.sel_pl().
 template <class Src>
 __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float beta, float two_d,
                         double r2, double D, double radius, int k, const Sel &S, int lane) {
@@ -344,14 +350,14 @@ __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float be
   const float r2lo = __double2float_rd(r2 - D);
   int flagged = 0;
   for (int p = lane; p < n_g; p += 32) {
-    const float ap = S.ga[p];
-    const int b = S.gb[p];
+    const float ap = S.ga()[p];
+    const int b = S.gb()[p];
     const float t = ap * inv_w;
     const float fr = t - floorf(t);
     const bool edge = fr < beta || fr > 1.0f - beta;
     const int lo = edge ? (b > 0 ? b - 1 : 0) : b;
     const int hi = edge ? (b < bmax ? b + 1 : bmax) : b;
-    const uint32_t hlo = S.hc[lo], hhi = S.hc[hi];
+    const uint32_t hlo = S.hc()[lo], hhi = S.hc()[hi];
     const int start = (int)(hlo >> 16) - (int)(hlo & 0xffffu);
     const int end = (int)(hhi >> 16);
     const float dlo = ap - two_d, dhi = ap + two_d;
@@ -359,14 +365,14 @@ __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float be
     // always inside the band: one band count is its own)
     int rank = start, nband = 0;
     for (int q = start; q < end; ++q) {
-      const float aq = S.ga[q];
+      const float aq = S.ga()[q];
       rank += aq < dlo ? 1 : 0;
       nband += (aq >= dlo && aq <= dhi) ? 1 : 0;
     }
     const bool amb = nband > 1;
     const uint8_t f = (amb ? 1 : 0) | (ap > r2lo ? 2 : 0) | (edge ? 8 : 0);
-    S.gf[p] = f;
-    if (!(f & 3) && rank < k) S.sel_pl[rank] = S.gpl[p];
+    S.gf()[p] = f;
+    if (!(f & 3) && rank < k) S.sel_pl()[rank] = S.gpl()[p];
     flagged += (f & 3) != 0;
   }
   int n_invalid = 0;
@@ -374,14 +380,14 @@ __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float be
     __syncwarp();
     // phase B: exact (distance, id) of the flagged elements
     for (int p = lane; p < n_g; p += 32) {
-      const uint8_t f = S.gf[p];
+      const uint8_t f = S.gf()[p];
       if (!(f & 3)) continue;
       int id;
-      const double e = src.exact(S.gpl[p], id);
-      S.ge[p] = e;
-      S.gid[p] = id;
+      const double e = src.exact(S.gpl()[p], id);
+      S.ge()[p] = e;
+      S.gid()[p] = id;
       if (e > radius) {
-        S.gf[p] = f | 4;
+        S.gf()[p] = f | 4;
         ++n_invalid;
       }
     }
@@ -389,30 +395,30 @@ __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float be
     // phase C: rank the valid flagged elements (near ties compared exactly;
     // ambiguity is symmetric, so both ends of a near tie carry exact keys)
     for (int p = lane; p < n_g; p += 32) {
-      const uint8_t f = S.gf[p];
+      const uint8_t f = S.gf()[p];
       if (!(f & 3) || (f & 4)) continue;
-      const float ap = S.ga[p];
-      const int b = S.gb[p];
+      const float ap = S.ga()[p];
+      const int b = S.gb()[p];
       const bool edge = f & 8;
       const int lo = edge ? (b > 0 ? b - 1 : 0) : b;
       const int hi = edge ? (b < bmax ? b + 1 : bmax) : b;
-      const uint32_t hlo = S.hc[lo], hhi = S.hc[hi];
+      const uint32_t hlo = S.hc()[lo], hhi = S.hc()[hi];
       const int start = (int)(hlo >> 16) - (int)(hlo & 0xffffu);
       const int end = (int)(hhi >> 16);
       const float dlo = ap - two_d, dhi = ap + two_d;
-      const double ep = S.ge[p];
-      const int ip = S.gid[p];
+      const double ep = S.ge()[p];
+      const int ip = S.gid()[p];
       int rank = start;
       for (int q = start; q < end; ++q) {
         if (q == p) continue;
-        const float aq = S.ga[q];
+        const float aq = S.ga()[q];
         if (aq < dlo) {
           ++rank;
         } else if (aq <= dhi) {
-          if (!(S.gf[q] & 4) && key_less(S.ge[q], S.gid[q], ep, ip)) ++rank;
+          if (!(S.gf()[q] & 4) && key_less(S.ge()[q], S.gid()[q], ep, ip)) ++rank;
         }
       }
-      if (rank < k) S.sel_pl[rank] = S.gpl[p];
+      if (rank < k) S.sel_pl()[rank] = S.gpl()[p];
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) n_invalid += __shfl_xor_sync(kFull, n_invalid, off);
@@ -455,9 +461,9 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
       const unsigned bal = __ballot_sync(kFull, ok);
       const int pos = n + __popc(bal & ((1u << lane) - 1u));
       if (ok && pos < S.gcap) {
-        S.ga[pos] = a;
-        S.gpl[pos] = pl;
-        S.gb[pos] = 0;
+        S.ga()[pos] = a;
+        S.gpl()[pos] = pl;
+        S.gb()[pos] = 0;
       }
       n += __popc(bal);
     });
@@ -473,14 +479,14 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
       // (non-negative float keys order like their bit patterns: one 64-bit
       // compare of (key bits, payload) per broadcast; near ties are found
       // afterwards between sorted neighbours, staged in the idle pass-1 buffer)
-      const float a = lane < n ? S.ga[lane] : INFINITY;
-      const int pl = lane < n ? S.gpl[lane] : 0x7fffffff;
+      const float a = lane < n ? S.ga()[lane] : INFINITY;
+      const int pl = lane < n ? S.gpl()[lane] : 0x7fffffff;
       const unsigned long long key =
           ((unsigned long long)__float_as_uint(a) << 32) | (unsigned long long)(unsigned)pl;
       int rank = 0;
 #pragma unroll 4
       for (int j = 0; j < n; ++j) rank += __shfl_sync(kFull, key, j) < key ? 1 : 0;
-      float *const srt = S.ca;
+      float *const srt = S.ca();
       if (lane < n) srt[rank] = a;
       __syncwarp();
       bool amb = false;
@@ -488,13 +494,13 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
         amb = (rank + 1 < n && srt[rank + 1] - a <= two_d) || (rank > 0 && a - srt[rank - 1] <= two_d);
       const bool bad = lane < n && rank < k && (amb || a > r2lo);
       if (!__any_sync(kFull, bad)) {
-        if (lane < n && rank < k) S.sel_pl[rank] = pl;
+        if (lane < n && rank < k) S.sel_pl()[rank] = pl;
         __syncwarp();
         return n < k ? n : k;
       }
     }
     if (n <= S.gcap && n <= 0xffff) {
-      if (lane == 0) S.hc[0] = ((uint32_t)n << 16) | (uint32_t)n;
+      if (lane == 0) S.hc()[0] = ((uint32_t)n << 16) | (uint32_t)n;
       __syncwarp();
       // one bucket: inv_w = 0 puts every key on the bucket "edge" -> window 0..0
       return rank_set(src, n, 0, 0.0f, beta, two_d, r2, D, radius, k, S, lane);
@@ -510,19 +516,19 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
   uint32_t cnt[kPer];
   int bstar, bmax, nbuf;
   static_assert(kPer == 8, "the histogram is read / written as two uint4 per lane");
-  uint4 *const hc4 = reinterpret_cast<uint4 *>(S.hc);
+  uint4 *const hc4 = reinterpret_cast<uint4 *>(S.hc());
   while (true) {
     hc4[lane] = make_uint4(0u, 0u, 0u, 0u);
     hc4[lane + 32] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
     nbuf = 0;
     src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
-      if (ok) atomicAdd(&S.hc[bucket_of(a, inv_w)], 1u);
+      if (ok) atomicAdd(&S.hc()[bucket_of(a, inv_w)], 1u);
       const unsigned bal = __ballot_sync(kFull, ok);
       const int pos = nbuf + __popc(bal & ((1u << lane) - 1u));
       if (ok && pos < S.ccap) {
-        S.ca[pos] = a;
-        S.cp[pos] = (uint16_t)(pl - pb);
+        S.ca()[pos] = a;
+        S.cp()[pos] = (uint16_t)(pl - pb);
       }
       nbuf += __popc(bal);
     });
@@ -575,7 +581,7 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
   hc4[2 * lane + 1] = make_uint4(hv[4], hv[5], hv[6], hv[7]);
   __syncwarp();
   {
-    const uint32_t hb = S.hc[bmax];   // (start << 16) | count of the last kept bucket
+    const uint32_t hb = S.hc()[bmax];   // (start << 16) | count of the last kept bucket
     n_g = (hb >> 16) + (hb & 0xffffu);
   }
   if (n_g > (uint32_t)S.gcap || total > 0xffffu) {
@@ -586,14 +592,14 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
   auto scatter = [&](float a, int pl) {
     const int b = bucket_of(a, inv_w);
     if (b <= bmax) {
-      const uint32_t pos = atomicAdd(&S.hc[b], 1u << 16) >> 16;
-      S.ga[pos] = a;
-      S.gpl[pos] = pl;
-      S.gb[pos] = (uint8_t)b;
+      const uint32_t pos = atomicAdd(&S.hc()[b], 1u << 16) >> 16;
+      S.ga()[pos] = a;
+      S.gpl()[pos] = pl;
+      S.gb()[pos] = (uint8_t)b;
     }
   };
   if (nbuf <= S.ccap && small) {
-    for (int p = lane; p < nbuf; p += 32) scatter(S.ca[p], pb + (int)S.cp[p]);
+    for (int p = lane; p < nbuf; p += 32) scatter(S.ca()[p], pb + (int)S.cp()[p]);
   } else {
     // only keys in buckets <= bmax matter: a < (bmax + 1) w, so d^2 < that + D
     if (bmax < kNB - 1) src.restrict_to(sqrt(((double)bmax + 1.01) * w + D) + 1e-6, lane);
@@ -650,16 +656,8 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
   const int64_t p0 = T.p_off[w];
   const int np = (int)(T.p_off[w + 1] - p0);
   Sel S;
-  S.hc = reinterpret_cast<uint32_t *>(wb + WL.hc);
-  S.ca = reinterpret_cast<float *>(wb + WL.ca);
-  S.cp = reinterpret_cast<uint16_t *>(wb + WL.cp);
-  S.ga = reinterpret_cast<float *>(wb + WL.ga);
-  S.ge = reinterpret_cast<double *>(wb + WL.ge);
-  S.gid = reinterpret_cast<int *>(wb + WL.gid);
-  S.gpl = reinterpret_cast<int *>(wb + WL.gpl);
-  S.gb = wb + WL.gb;
-  S.gf = wb + WL.gf;
-  S.sel_pl = reinterpret_cast<int *>(wb + WL.sel_pl);
+  S.wb = wb;
+  S.L = WL;
   S.gcap = gcap_of(cap_a, cap_r);
   S.ccap = SharedPts ? kCandShared : kCandGlobal;
   float *const row0 = reinterpret_cast<float *>(wb + WL.row);
@@ -733,7 +731,7 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
     const int ma = select_topk<true>(psrc, cap_a, radius, D_fp64, S, lane, radius, no_bound);
     float *ps = row + 7;
     for (int m = lane; m < ma; m += 32) {
-      const int j = S.sel_pl[m];
+      const int j = S.sel_pl()[m];
       const double dx = ax[j] - px, dy = ay[j] - py;
       float *slot = ps + 7 * m;
       slot[0] = (float)(dx * ch + dy * sh);
@@ -793,7 +791,7 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
     for (int m = lane; m < cap_r; m += 32) {
       float *slot = rstage + 11 * m;
       if (m < mr) {
-        const int s = S.sel_pl[m] + sel_off;
+        const int s = S.sel_pl()[m] + sel_off;
         double qx, qy, qh;
         int kind, qid;
         if (SharedPts) {
