@@ -161,8 +161,8 @@ __device__ __forceinline__ void reset_agent(const ds_tables &T, const ds_state &
 
 // MAXT: the launch's thread bound (worlds of <= 256 agents get the 256
 // variant: up to 255 registers, no spills of the FP64 state)
-template <int MAXT>
-__global__ void __launch_bounds__(MAXT) step_kernel(ds_tables T, ds_config C, ds_state S,
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) step_kernel(ds_tables T, ds_config C, ds_state S,
                                                     ds_step_args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int w = blockIdx.x;
@@ -432,20 +432,26 @@ __global__ void __launch_bounds__(1024) reset_kernel(ds_tables T, ds_state S, co
 }
 
 cudaError_t configure_step_kernels(int max_dynamic_smem) {
-  cudaError_t e = cudaFuncSetAttribute(step_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       max_dynamic_smem);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(step_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              max_dynamic_smem);
+  const void *ks[] = {(const void *)step_kernel<128, 8>, (const void *)step_kernel<256, 1>,
+                      (const void *)step_kernel<1024, 1>};
+  for (const void *k : ks) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         max_dynamic_smem);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_step(const ds_handle *h, const ds_step_args *a, cudaStream_t s) {
-  if (h->step_threads <= 256)
-    step_kernel<256><<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg, h->st,
-                                                                           *a);
+  if (h->step_threads <= 128)   // 8 CTAs (32 warps) per SM at <= 64 registers
+    step_kernel<128, 8><<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg,
+                                                                              h->st, *a);
+  else if (h->step_threads <= 256)
+    step_kernel<256, 1><<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg,
+                                                                              h->st, *a);
   else
-    step_kernel<1024><<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg, h->st,
-                                                                            *a);
+    step_kernel<1024, 1><<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg,
+                                                                               h->st, *a);
   return cudaGetLastError();
 }
 
