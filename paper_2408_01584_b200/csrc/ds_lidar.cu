@@ -45,7 +45,14 @@ __host__ __device__ inline size_t lidar_agents_bytes(int amax) {
 constexpr size_t kSegCacheBytes = 32 * (4 * sizeof(double) + 1);
 __host__ __device__ inline size_t lidar_warp_bytes(int obs_width, int n_rays) {
   return al16l((size_t)n_rays * 5 * sizeof(double) + al16l(kSegCacheBytes) +
-               (size_t)obs_width * sizeof(float) + 16);
+               al16l((size_t)n_rays * sizeof(float)) + (size_t)obs_width * sizeof(float) + 16);
+}
+
+// Upper bound of asin(x) for 0 <= x (tan(asin x) = x / sqrt(1 - x^2) >=
+// asin x), pi/2 and above for x >= 0.95: conservative angular half-spans
+// without the cost of asinf
+__device__ __forceinline__ float asin_upper(float x) {
+  return x < 0.95f ? x * rsqrtf(1.0f - x * x) * (1.0f + 1e-6f) : 1.5708f;
 }
 
 constexpr double kInvTwoPi = 0.15915494309189535;
@@ -242,8 +249,13 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
   double *seg_ax = reinterpret_cast<double *>(rseg + C.n_rays);
   double *seg_ay = seg_ax + 32, *seg_bx = seg_ax + 64, *seg_by = seg_ax + 96;
   uint8_t *seg_ne = reinterpret_cast<uint8_t *>(seg_ax + 128);
+  // per-ray float upper bound of the road search bound (limit / best segment
+  // hit), rounded up: the cell culling and the walk's stop test read it
+  float *rbf = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(seg_ax) +
+                                         al16l(kSegCacheBytes));
   float *const row0 = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(seg_ax) +
-                                                al16l(kSegCacheBytes));
+                                                al16l(kSegCacheBytes) +
+                                                al16l((size_t)C.n_rays * sizeof(float)));
   const int row0_phase = (int)((reinterpret_cast<uintptr_t>(row0) >> 2) & 3);
 
   const int64_t a0 = T.a_off[w];
@@ -323,7 +335,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
           int k_hi = R - 1;
           const float dist = sqrtf(d2);
           if (dist > cr + 1e-3f) {
-            const float half = asinf(fminf(1.0f, cr / dist)) + 1e-4f;
+            const float half = asin_upper(cr / dist) + 1e-4f;
             float rel = fast_atan2(cy, cx) - half - fcenter;
             rel -= (float)kTwoPi * floorf(rel * (float)kInvTwoPi);   // [0, 2pi)
             ray_range(rel, 2.0f * half, full_circle, R, C.fov, k_lo, k_hi);
@@ -352,6 +364,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
     for (int k = lane; k < R; k += 32) {
       rlim[k] = fmin(__longlong_as_double((long long)rbest[k]), max_range) * (1.0 + 1e-12) + 1e-9;
       rseg[k] = 0xffffffffffffffffull;
+      rbf[k] = __double2float_ru(rlim[k]);
     }
     __syncwarp();
     // road segments, segment-major, grid cells in Chebyshev rings around the
@@ -393,16 +406,15 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
               // origin is at least 1.5 cells from the cell centre)
               const float ccx = xlo + 0.5f * fcs - fox, ccy = ylo + 0.5f * fcs - foy;
               const float dc = sqrtf(ccx * ccx + ccy * ccy);
-              const float half = asinf(fminf(1.0f, cell_rad / dc)) + 1e-4f;
+              const float half = asin_upper(cell_rad / dc) + 1e-4f;
               float rel = fast_atan2(ccy, ccx) - half - fcenter;
               rel -= (float)kTwoPi * floorf(rel * (float)kInvTwoPi);
               int k_lo, k_hi;
               ray_range(rel, 2.0f * half, full_circle, R, C.fov, k_lo, k_hi);
-              const double need = (double)dmin;
               keep = false;
               for (int m = k_lo; m <= k_hi && !keep; ++m) {
                 const int k = m >= R ? m - R : m;
-                keep = !(ray_bound(rlim[k], rseg[k]) < need);
+                keep = !(rbf[k] < dmin);
               }
             }
             if (keep) {
@@ -453,9 +465,13 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
               const double beat = ray_bound(lim, rseg[k]);
               const double t = ray_segment(ox, oy, rdx[k], rdy[k], seg_ax[owner], seg_ay[owner],
                                            seg_bx[owner], seg_by[owner], beat);
-              if (t <= lim)
+              if (t <= lim) {
                 atomicMin(&rseg[k], ((unsigned long long)__double_as_longlong(t + 0.0) << 1) |
                                         (unsigned long long)seg_ne[owner]);
+                // non-negative floats order like their bits
+                atomicMin(reinterpret_cast<unsigned *>(rbf) + k,
+                          __float_as_uint(__double2float_ru(t + 0.0)));
+              }
             }
           }
           __syncwarp();
@@ -471,7 +487,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
           const double far = (rrem - 1) * cs - 1e-6;
           bool open = false;
           #pragma unroll 1
-          for (int k = lane; k < R; k += 32) open = open || !(ray_bound(rlim[k], rseg[k]) < far);
+          for (int k = lane; k < R; k += 32) open = open || !((double)rbf[k] < far);
           if (!__any_sync(kFullMask, open)) break;
         }
       }
