@@ -487,7 +487,8 @@ def main():
                     "bytes_per_agent_step": bpa["obs_kernel"], "peak_kind": peak_kind}
     if rank == 0:
         cpu = None
-        if not args.no_cpu_baseline:
+        # the CPU baseline leg runs at N = 1 only (rank 0); N > 1 lines reuse it
+        if not args.no_cpu_baseline and world == 1:
             threads = os.cpu_count() or 1
             try:
                 v, sample = CpuSample(args.config, threads).rate(91, warmup=1, budget_s=20.0,
