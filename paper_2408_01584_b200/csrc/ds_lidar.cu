@@ -70,16 +70,19 @@ __device__ __forceinline__ float fast_atan2(float y, float x) {
   return y < 0.0f ? -r : r;
 }
 
-// Ray indices whose direction can lie in the angular interval [rel, rel +
-// span] (rel in [0, 2pi) relative to the sweep centre, already widened):
+// Ray indices whose direction lies in the angular interval [rel, rel + span]
+// (rel in [0, 2pi) relative to the sweep centre, widened by the callers far
+// beyond the float error of rel, so the tight ceil / floor range is safe):
 // full circle rays at 2 pi k / R (range may run past R - 1, callers wrap),
 // cone rays at -fov/2 + fov k / (R - 1) (interval tried at rel and rel - 2pi).
 __device__ __forceinline__ void ray_range(float rel, float span, bool full, int R, double fov,
                                           int &k_lo, int &k_hi) {
   if (full) {
+    // only rays whose direction lies inside the (already widened) interval:
+    // ceil / floor, possibly empty (k_hi < k_lo)
     const float scl = (float)R * (float)kInvTwoPi;
-    k_lo = (int)floorf(rel * scl);
-    k_hi = (int)ceilf((rel + span) * scl);
+    k_lo = (int)ceilf(rel * scl);
+    k_hi = (int)floorf((rel + span) * scl);
     if (k_hi - k_lo + 1 >= R) {
       k_lo = 0;
       k_hi = R - 1;
@@ -95,8 +98,8 @@ __device__ __forceinline__ void ray_range(float rel, float span, bool full, int 
   int lo = R, hi = -1;
   for (int sh = 0; sh < 2; ++sh) {
     const float rr = sh == 0 ? rel : rel - (float)kTwoPi;
-    const int a2 = max((int)floorf((rr + hf) * scl), 0);
-    const int b2 = min((int)ceilf((rr + span + hf) * scl), R - 1);
+    const int a2 = max((int)ceilf((rr + hf) * scl), 0);
+    const int b2 = min((int)floorf((rr + span + hf) * scl), R - 1);
     if (a2 <= b2) {
       lo = min(lo, a2);
       hi = max(hi, b2);
