@@ -44,7 +44,7 @@ __host__ __device__ inline size_t lidar_agents_bytes(int amax) {
 // shifted by up to 3 floats to the output's phase)
 constexpr size_t kSegCacheBytes = 32 * (4 * sizeof(double) + 1);
 __host__ __device__ inline size_t lidar_warp_bytes(int obs_width, int n_rays) {
-  return al16l((size_t)n_rays * 5 * sizeof(double) + al16l(kSegCacheBytes) +
+  return al16l((size_t)n_rays * 5 * sizeof(double) + al16l(kSegCacheBytes) + 32 * sizeof(int) +
                al16l((size_t)n_rays * sizeof(float)) + (size_t)obs_width * sizeof(float) + 16);
 }
 
@@ -254,10 +254,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
   uint8_t *seg_ne = reinterpret_cast<uint8_t *>(seg_ax + 128);
   // per-ray float upper bound of the road search bound (limit / best segment
   // hit), rounded up: the cell culling and the walk's stop test read it
-  float *rbf = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(seg_ax) +
-                                         al16l(kSegCacheBytes));
+  int *fscr = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(seg_ax) +
+                                      al16l(kSegCacheBytes));   // FlatRows compaction
+  float *rbf = reinterpret_cast<float *>(fscr + 32);
   float *const row0 = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(seg_ax) +
-                                                al16l(kSegCacheBytes) +
+                                                al16l(kSegCacheBytes) + 32 * sizeof(int) +
                                                 al16l((size_t)C.n_rays * sizeof(float)));
   const int row0_phase = (int)((reinterpret_cast<uintptr_t>(row0) >> 2) & 3);
 
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
         }
       }
       FlatRows pairs;
-      pairs.build(k_lo, n_k, lane);
+      pairs.build(k_lo, n_k, lane, fscr);
       for (int p0 = 0; p0 < pairs.total; p0 += 32) {
         int owner;
         const int m = pairs.map_owner(p0, lane, owner);
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
           }
         }
         FlatRows cells;
-        cells.build(sb, cnt, lane);
+        cells.build(sb, cnt, lane, fscr);
         for (int f0 = 0; f0 < cells.total; f0 += 32) {
           const int e = cells.map(f0, lane);
           int k_lo = 0, n_k = 0;
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
           }
           __syncwarp();
           FlatRows pairs;
-          pairs.build(k_lo, n_k, lane);
+          pairs.build(k_lo, n_k, lane, fscr);
           for (int p0 = 0; p0 < pairs.total; p0 += 32) {
             int owner;
             const int m = pairs.map_owner(p0, lane, owner);

@@ -96,6 +96,28 @@ struct FlatRows {
     const int r = (r0 + __popc(E & ((2u << lane) - 1u))) & 31;
     return __shfl_sync(kFullMask, base, r) + f0 + lane;
   }
+  // build() with the compaction through 32 ints of per-warp shared scratch
+  // (each non-empty lane stores its lane id at its compacted slot) instead
+  // of a find-n-th-set-bit per lane
+  __device__ __forceinline__ void build(int sb_in, int cnt_in, int lane, int *scratch) {
+    const unsigned bal = __ballot_sync(kFullMask, cnt_in > 0);
+    nr = __popc(bal);
+    __syncwarp();
+    if (cnt_in > 0) scratch[__popc(bal & ((1u << lane) - 1u))] = lane;
+    __syncwarp();
+    src = lane < nr ? scratch[lane] : 0;
+    sb = __shfl_sync(kFullMask, sb_in, src);
+    cnt = __shfl_sync(kFullMask, cnt_in, src);
+    if (lane >= nr) cnt = 0;
+    pe = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int up = __shfl_up_sync(kFullMask, pe, off);
+      if (lane >= off) pe += up;
+    }
+    total = __shfl_sync(kFullMask, pe, 31);
+    base = sb - (pe - cnt);
+  }
   // as map(), also returning the original lane that owned the range
   __device__ __forceinline__ int map_owner(int f0, int lane, int &owner) const {
     const bool live = lane < nr;
