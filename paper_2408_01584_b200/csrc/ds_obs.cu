@@ -59,7 +59,7 @@ __host__ __device__ constexpr size_t al16(size_t v) { return (v + 15) & ~size_t(
 // selection has produced sel_pl.  constexpr: with compile-time slot caps the
 // whole layout folds into immediate offsets off one base register.
 struct WarpLayout {
-  size_t row, hc, ca, cp, ga, ge, gid, gpl, gb, gf, sel_pl, total;
+  size_t row, hc, ca, cp, ga, ge, gid, gpl, gb, gf, sel_pl, fr, total;
 };
 
 __host__ __device__ constexpr WarpLayout make_layout(int cap_a, int cap_r, bool buffered) {
@@ -95,6 +95,7 @@ __host__ __device__ constexpr WarpLayout make_layout(int cap_a, int cap_r, bool 
   const size_t road_end = al16(L.hc + (size_t)cap_r * 11 * sizeof(float));
   if (o < road_end) o = road_end;
   L.sel_pl = o; o = al16(o + km * sizeof(int));
+  L.fr = o; o = al16(o + 32 * sizeof(int));   // FlatRows compaction scratch
   L.total = o;
   return L;
 }
@@ -188,11 +189,12 @@ struct RoadSrcShared {
   float prx, pry;
   double px, py;
   const RowGeo *geo;
+  int *fscr;
   FlatRows rows;
   __device__ __forceinline__ void cover(double rho, int lane) {
     int b, c;
     geo->range((float)rho, lane, b, c);
-    rows.build(b - p0, c, lane);
+    rows.build(b - p0, c, lane, fscr);
   }
   __device__ __forceinline__ void restrict_to(double rho, int lane) { cover(rho, lane); }
   __device__ __forceinline__ int pbase() const { return 0; }
@@ -225,11 +227,12 @@ struct RoadSrcGlobal {
   int p0, np;
   double px, py;
   const RowGeo *geo;
+  int *fscr;
   FlatRows rows;
   __device__ __forceinline__ void cover(double rho, int lane) {
     int b, c;
     geo->range((float)rho, lane, b, c);
-    rows.build(b, c, lane);
+    rows.build(b, c, lane, fscr);
   }
   __device__ __forceinline__ void restrict_to(double rho, int lane) { cover(rho, lane); }
   __device__ __forceinline__ int pbase() const { return p0; }
@@ -772,12 +775,13 @@ __global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kern
         const double D = 4.0 * (radius + 1.0) * E + 2.0 * E * E + D_fp64;
         const double rho = hint_radius(rho_hint, radius, D);
         RoadSrcShared rsrc{pts, static_cast<const ds_point_rec *>(T.gpt_rec), (int)p0, prx, pry, px,
-                           py, &geo};
+                           py, &geo, reinterpret_cast<int *>(wb + WL.fr)};
         rsrc.cover(rho < radius ? rho : reach, lane);
         mr = select_topk<false>(rsrc, cap_r, radius, D, S, lane, rho, bound);
       } else {
         const double rho = hint_radius(rho_hint, radius, D_fp64);
-        RoadSrcGlobal rsrc{T.gpt_x, T.gpt_y, T.gpt_id, (int)p0, np, px, py, &geo};
+        RoadSrcGlobal rsrc{T.gpt_x, T.gpt_y, T.gpt_id, (int)p0, np, px, py, &geo,
+                           reinterpret_cast<int *>(wb + WL.fr)};
         rsrc.cover(rho < radius ? rho : reach, lane);
         mr = select_topk<false>(rsrc, cap_r, radius, D_fp64, S, lane, rho, bound);
       }
