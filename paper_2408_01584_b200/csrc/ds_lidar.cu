@@ -268,8 +268,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
     const int64_t g = a0 + i;
     sx[i] = St.x[g];
     sy[i] = St.y[g];
-    sc[i] = cos(St.heading[g]);
-    ss[i] = sin(St.heading[g]);
+    sincos(St.heading[g], &ss[i], &sc[i]);
     shl[i] = T.half_l[g];
     shw[i] = T.half_w[g];
     scr[i] = T.circumradius[g];
@@ -482,11 +481,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
         }
         // the remaining cells lie in rings >= ring_of(q0 + 32), at least
         // (that ring - 1) cells from the origin's cell
-        int rrem = 0;
-        if (q0 + 32 < n_cells) {
-          int dxr, dyr;
-          ring_cell(q0 + 32, table, dxr, dyr, rrem);
-        }
+        const int rrem = q0 + 32 < n_cells ? ring_of(q0 + 32) : 0;   // warp-uniform
         if (rrem >= 2) {
           const double far = (rrem - 1) * cs - 1e-6;
           bool open = false;
