@@ -14,8 +14,8 @@
 //          absolute error bound D; a 256-bucket histogram of a over
 //          [0, r^2 + D] gives the threshold bucket b* (first bucket whose
 //          cumulative count reaches k);
-//  pass 2  candidates in buckets <= b*+2 are counting-sort scattered into a
-//          small set G (about k+3 entries);
+//  pass 2  candidates in buckets <= b*+1 are counting-sort scattered into a
+//          small set G (about k+1 entries);
 //  exact   only G gets the glibc-exact FP64 hypot (ds_math.cuh), the exact
 //          radius test and an exact (d, id) rank.  Since |a - d^2| <= D, key
 //          order inversions only involve ADJACENT buckets and only keys within
@@ -330,7 +330,7 @@ __device__ __forceinline__ double sel_r2hi(double radius, double D) {
 // Radius that provably contains the k nearest candidates given a hint that
 // bounds the k-th distance (triangle inequality).  The narrowed selection
 // histograms [0, rho^2] (bucket width w = rho^2 / kNB); the k-th key is
-// <= hint^2 + D, so the bucket window b* + 2 (+1.01 slack) stays inside
+// <= hint^2 + D, so the bucket window b* + 1 (+1.01 slack) stays inside
 // rho^2 - D when rho^2 (1 - 3.05 / kNB) >= hint^2 + 2D.  The floor
 // rho^2 >= 10240 D keeps the edge band beta = 2 D kNB / rho^2 <= 0.05.
 // (float arithmetic: any radius is correct here, the caller validates the
@@ -560,7 +560,10 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) bstar = min(bstar, __shfl_xor_sync(kFull, bstar, off));
-    bmax = min(bstar + 2, kNB - 1);
+    // G = buckets <= b*+1: an element of b*+1 reaches rank < k only through an
+    // inversion with b* at their shared edge, and its window never needs
+    // b*+2 (all of b*+2 lies above it); edge windows are clamped to bmax
+    bmax = min(bstar + 1, kNB - 1);
     // a narrowed scan is valid only if all buckets <= bmax lie inside the disc
     if (restricted && !((((double)bmax + 1.01) * w + D) <= rho * rho)) {
       src.restrict_to(radius + 1e-6, lane);
