@@ -331,14 +331,14 @@ __device__ __forceinline__ double sel_r2hi(double radius, double D) {
 // bounds the k-th distance (triangle inequality).  The narrowed selection
 // histograms [0, rho^2] (bucket width w = rho^2 / kNB); the k-th key is
 // <= hint^2 + D, so the bucket window b* + 1 (+1.01 slack) stays inside
-// rho^2 - D when rho^2 (1 - 3.05 / kNB) >= hint^2 + 2D.  The floor
+// rho^2 - D when rho^2 (1 - 2.05 / kNB) >= hint^2 + 2D.  The floor
 // rho^2 >= 10240 D keeps the edge band beta = 2 D kNB / rho^2 <= 0.05.
 // (float arithmetic: any radius is correct here, the caller validates the
 // narrowed window against the rho it actually uses)
 __device__ __forceinline__ double hint_radius(float hint, double radius, double D) {
   if (!(hint > 0.0f)) return radius;
   const float Df = (float)D;
-  const float r2n = fmaxf((hint * hint + 2.0f * Df) * (1.0f / (1.0f - 3.05f / kNB)) + 1e-3f,
+  const float r2n = fmaxf((hint * hint + 2.0f * Df) * (1.0f / (1.0f - 2.05f / kNB)) + 1e-3f,
                           10240.0f * Df);
   return fmin((double)sqrtf(r2n), radius);
 }
