@@ -59,7 +59,7 @@ __host__ __device__ constexpr size_t al16(size_t v) { return (v + 15) & ~size_t(
 // selection has produced sel_pl.  constexpr: with compile-time slot caps the
 // whole layout folds into immediate offsets off one base register.
 struct WarpLayout {
-  size_t row, hc, ca, cp, ga, ge, gid, gpl, gb, gf, sel_pl, fr, total;
+  size_t row, hc, ca, cp, ga, ge, gid, gpl, gf, sel_pl, fr, total;
 };
 
 __host__ __device__ constexpr WarpLayout make_layout(int cap_a, int cap_r, bool buffered) {
@@ -90,7 +90,6 @@ __host__ __device__ constexpr WarpLayout make_layout(int cap_a, int cap_r, bool 
     L.gid = o; o = al16(o + gc * sizeof(int));
   }
   L.gpl = o; o = al16(o + gc * sizeof(int));
-  L.gb = o; o = al16(o + gc);
   L.gf = o; o = al16(o + gc);
   const size_t road_end = al16(L.hc + (size_t)cap_r * 11 * sizeof(float));
   if (o < road_end) o = road_end;
@@ -131,7 +130,6 @@ struct Sel {
   __device__ __forceinline__ double *ge() const { return reinterpret_cast<double *>(wb + L.ge); }
   __device__ __forceinline__ int *gid() const { return reinterpret_cast<int *>(wb + L.gid); }
   __device__ __forceinline__ int *gpl() const { return reinterpret_cast<int *>(wb + L.gpl); }
-  __device__ __forceinline__ uint8_t *gb() const { return wb + L.gb; }
   __device__ __forceinline__ uint8_t *gf() const { return wb + L.gf; }
   __device__ __forceinline__ int *sel_pl() const { return reinterpret_cast<int *>(wb + L.sel_pl); }
 };
@@ -354,8 +352,8 @@ __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float be
   int flagged = 0;
   for (int p = lane; p < n_g; p += 32) {
     const float ap = S.ga()[p];
-    const int b = S.gb()[p];
     const float t = ap * inv_w;
+    const int b = min((int)t, kNB - 1);   // = bucket_of(ap, inv_w), the scatter's bucket
     const float fr = t - floorf(t);
     const bool edge = fr < beta || fr > 1.0f - beta;
     const int lo = edge ? (b > 0 ? b - 1 : 0) : b;
@@ -401,7 +399,7 @@ __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float be
       const uint8_t f = S.gf()[p];
       if (!(f & 3) || (f & 4)) continue;
       const float ap = S.ga()[p];
-      const int b = S.gb()[p];
+      const int b = bucket_of(ap, inv_w);
       const bool edge = f & 8;
       const int lo = edge ? (b > 0 ? b - 1 : 0) : b;
       const int hi = edge ? (b < bmax ? b + 1 : bmax) : b;
@@ -466,7 +464,6 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
       if (ok && pos < S.gcap) {
         S.ga()[pos] = a;
         S.gpl()[pos] = pl;
-        S.gb()[pos] = 0;
       }
       n += __popc(bal);
     });
@@ -601,7 +598,6 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
       const uint32_t pos = atomicAdd(&S.hc()[b], 1u << 16) >> 16;
       S.ga()[pos] = a;
       S.gpl()[pos] = pl;
-      S.gb()[pos] = (uint8_t)b;
     }
   };
   if (nbuf <= S.ccap && small) {
