@@ -40,6 +40,11 @@ constexpr int kCandShared = 224;  // (shared-points variant: hint-narrowed scans
 // 2.53 / 2.28 / 2.16 ms at C3); 32 fits the default caps with 10k points
 constexpr int kWarpsShared = 32;
 constexpr int kWarpsSharedSmall = 24;
+// batches of >= 2 x #SMs worlds of <= 64 agents whose tables fit twice per
+// SM: two 16-warp CTAs per SM (the same 32 warps, but one world's staging
+// overlaps the other's rows; C2 obs 0.193 -> 0.190 ms)
+constexpr int kWarpsSharedPair = 16;
+constexpr int kSmemPerSM = 228 * 1024;
 constexpr int kWarpsGlobal = 12;
 
 __host__ __device__ constexpr int kmax_of(int cap_a, int cap_r) {
@@ -626,7 +631,7 @@ struct RadialK {
 };
 
 template <int WARPS, bool SharedPts, int CAPA, int CAPR>
-__global__ void __launch_bounds__(WARPS * 32, SharedPts ? 1 : 2) obs_radial_kernel(
+__global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 1) obs_radial_kernel(
     ds_tables T, ds_config C, ds_state St, const RadialK K, const uint8_t *mask, const ObsOut O,
     const float *scale, int32_t *sel_idx, int obs_width) {
   const int w = blockIdx.x;
@@ -839,6 +844,8 @@ cudaError_t configure_kernels(int max_dynamic_smem) {
                       (const void *)obs_radial_kernel<kWarpsShared, true, 0, 0>,
                       (const void *)obs_radial_kernel<kWarpsSharedSmall, true, 16, 64>,
                       (const void *)obs_radial_kernel<kWarpsSharedSmall, true, 0, 0>,
+                      (const void *)obs_radial_kernel<kWarpsSharedPair, true, 16, 64>,
+                      (const void *)obs_radial_kernel<kWarpsSharedPair, true, 0, 0>,
                       (const void *)obs_radial_kernel<kWarpsGlobal, false, 16, 64>,
                       (const void *)obs_radial_kernel<kWarpsGlobal, false, 0, 0>};
   for (const void *k : ks) {
@@ -862,7 +869,14 @@ void obs_plan(ds_handle *h, int max_optin) {
   const size_t sh = obs_smem_bytes_shared(h->cfg, h->tab.max_agents, h->tab.max_points, kWarpsShared);
   const size_t sh_small =
       obs_smem_bytes_shared(h->cfg, h->tab.max_agents, h->tab.max_points, kWarpsSharedSmall);
-  if (can && sh <= (size_t)max_optin) {
+  const size_t sh_pair =
+      obs_smem_bytes_shared(h->cfg, h->tab.max_agents, h->tab.max_points, kWarpsSharedPair);
+  if (can && h->tab.max_agents <= 64 && h->tab.n_worlds >= 2 * h->num_sms &&
+      2 * (sh_pair + 1024) <= (size_t)kSmemPerSM) {
+    h->obs_shared_pts = 1;
+    h->obs_warps = kWarpsSharedPair;
+    h->obs_smem = sh_pair;
+  } else if (can && sh <= (size_t)max_optin) {
     h->obs_shared_pts = 1;
     h->obs_warps = kWarpsShared;
     h->obs_smem = sh;
@@ -875,6 +889,29 @@ void obs_plan(ds_handle *h, int max_optin) {
     h->obs_warps = kWarpsGlobal;
     h->obs_smem = obs_smem_bytes_global(h->cfg, h->tab.max_agents);
   }
+}
+
+struct ObsLaunch {
+  const ds_handle *h;
+  RadialK K;
+  const uint8_t *mask;
+  ObsOut O;
+  const float *scale;
+  int32_t *sel_idx;
+  int W;
+  bool fixed;
+  cudaStream_t s;
+};
+
+template <int WARPS, bool SharedPts>
+void launch_radial(const ObsLaunch &L) {
+  const ds_handle *h = L.h;
+  if (L.fixed)
+    obs_radial_kernel<WARPS, SharedPts, 16, 64><<<L.W, WARPS * 32, h->obs_smem, L.s>>>(
+        h->tab, h->cfg, h->st, L.K, L.mask, L.O, L.scale, L.sel_idx, h->obs_width);
+  else
+    obs_radial_kernel<WARPS, SharedPts, 0, 0><<<L.W, WARPS * 32, h->obs_smem, L.s>>>(
+        h->tab, h->cfg, h->st, L.K, L.mask, L.O, L.scale, L.sel_idx, h->obs_width);
 }
 
 cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, void *obs,
@@ -894,30 +931,11 @@ cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, void *obs,
   K.cs = h->cfg.grid_cell;
   K.inv_cs = 1.0 / K.cs;
   K.key_e = (K.radius + 1.0) * 1.2e-7;
-  if (h->obs_shared_pts && h->obs_warps == kWarpsShared) {
-    if (fixed)
-      obs_radial_kernel<kWarpsShared, true, 16, 64><<<W, kWarpsShared * 32, h->obs_smem, s>>>(
-          h->tab, h->cfg, h->st, K, mask, O, scale, sel_idx, h->obs_width);
-    else
-      obs_radial_kernel<kWarpsShared, true, 0, 0><<<W, kWarpsShared * 32, h->obs_smem, s>>>(
-          h->tab, h->cfg, h->st, K, mask, O, scale, sel_idx, h->obs_width);
-  } else if (h->obs_shared_pts) {
-    if (fixed)
-      obs_radial_kernel<kWarpsSharedSmall, true, 16, 64>
-          <<<W, kWarpsSharedSmall * 32, h->obs_smem, s>>>(h->tab, h->cfg, h->st, K, mask, O, scale,
-                                                         sel_idx, h->obs_width);
-    else
-      obs_radial_kernel<kWarpsSharedSmall, true, 0, 0>
-          <<<W, kWarpsSharedSmall * 32, h->obs_smem, s>>>(h->tab, h->cfg, h->st, K, mask, O, scale,
-                                                         sel_idx, h->obs_width);
-  } else {
-    if (fixed)
-      obs_radial_kernel<kWarpsGlobal, false, 16, 64><<<W, kWarpsGlobal * 32, h->obs_smem, s>>>(
-          h->tab, h->cfg, h->st, K, mask, O, scale, sel_idx, h->obs_width);
-    else
-      obs_radial_kernel<kWarpsGlobal, false, 0, 0><<<W, kWarpsGlobal * 32, h->obs_smem, s>>>(
-          h->tab, h->cfg, h->st, K, mask, O, scale, sel_idx, h->obs_width);
-  }
+  const ObsLaunch L{h, K, mask, O, scale, sel_idx, W, fixed, s};
+  if (!h->obs_shared_pts) launch_radial<kWarpsGlobal, false>(L);
+  else if (h->obs_warps == kWarpsShared) launch_radial<kWarpsShared, true>(L);
+  else if (h->obs_warps == kWarpsSharedSmall) launch_radial<kWarpsSharedSmall, true>(L);
+  else launch_radial<kWarpsSharedPair, true>(L);
   return cudaGetLastError();
 }
 

@@ -36,6 +36,9 @@ CASES = {
                    dict(obs=ObsConfig(max_agents_obs=3, max_road_points_obs=5, radius=30.0))),
     "big_caps": (dict(n_worlds=4, n_agents=100, n_points=6000),
                  dict(obs=ObsConfig(max_agents_obs=128, max_road_points_obs=128, radius=80.0))),
+    # >= 2 x 148 worlds of <= 64 agents: the two-CTAs-per-SM observation variant
+    "many_small_worlds": (dict(n_worlds=300, n_agents=24, n_points=300),
+                          dict(collision_behavior="remove_agent")),
     # 129..256 agents: the 256-thread step kernel variant
     "agents_200": (dict(n_worlds=3, n_agents=200, n_points=2000),
                    dict(collision_behavior="remove_agent")),
