@@ -25,9 +25,26 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 }
 
 // uniform in (0, 1): 24 random bits, centred in their cell
-__device__ __forceinline__ float hash_uniform(uint64_t key, uint64_t r, uint32_t j) {
-  const uint64_t h = mix64(key ^ mix64(r * 0x9e3779b97f4a7c15ull + j));
-  return ((float)(uint32_t)(h >> 40) + 0.5f) * 5.9604644775390625e-8f;
+// 32-bit integer hash (lowbias32): one per logit; the 64-bit key and the row
+// are folded into a per-row seed once
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+__device__ __forceinline__ uint32_t row_seed(uint64_t key, uint64_t r) {
+  return hash32((uint32_t)key ^ hash32((uint32_t)(key >> 32) ^ hash32((uint32_t)r) ^
+                                       (uint32_t)(r >> 32)));
+}
+
+// uniform in (0, 1): the top 24 bits, centred
+__device__ __forceinline__ float hash_uniform(uint32_t seed, uint32_t j) {
+  const uint32_t h = hash32(seed + j * 0x9e3779b9u);
+  return ((float)(h >> 8) + 0.5f) * 5.9604644775390625e-8f;
 }
 
 template <typename T>
@@ -49,9 +66,11 @@ __global__ void __launch_bounds__(kSampleWarps * 32) sample_kernel(const T *logi
   const T *row = logits + r * ld;
   float best = -INFINITY;
   int arg = 0x7fffffff;
+  const uint32_t seed = row_seed(key, (uint64_t)r);
   for (int j = lane; j < n; j += 32) {
-    const float u = hash_uniform(key, (uint64_t)r, (uint32_t)j);
-    const float v = load_logit(row + j) - logf(-logf(u));
+    const float u = hash_uniform(seed, (uint32_t)j);
+    // Gumbel noise -log(-log u) with the hardware log2 (u in (0, 1): -log u > 0)
+    const float v = load_logit(row + j) - __logf(-__logf(u));
     if (v > best || (v == best && j < arg) || arg == 0x7fffffff) {
       best = v;
       arg = j;
