@@ -382,7 +382,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
       const int ocx = (int)fmin(fmax(floor((ox - gx0) * inv_cs), -1e6), 1e6);
       const int ocy = (int)fmin(fmax(floor((oy - gy0) * inv_cs), -1e6), 1e6);
       const double reach = max_range + 1e-6;
-      const int rmax = (int)ceil(reach * inv_cs) + 1;
+      // a cell of ring r lies >= (r - 1) cells from the origin's cell
+      const int rmax = (int)floor(reach * inv_cs) + 1;
       const int n_cells = (2 * rmax + 1) * (2 * rmax + 1);
       const float cell_rad = (float)(cs * 0.7071067811865476) + 1e-3f;
       const bool table = rmax <= kRingTableR;
