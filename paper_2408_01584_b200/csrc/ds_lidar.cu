@@ -63,8 +63,14 @@ __device__ __forceinline__ float fast_atan2(float y, float x) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float a = __fdividef(fminf(ax, ay), fmaxf(ax, ay));
   const float s = a * a;
-  float r = a * (0.99997726f + s * (-0.33262347f + s * (0.19354346f + s * (-0.11643287f +
-                s * (0.05265332f + s * -0.01172120f)))));
+  // explicit FMAs: the library builds with --fmad=false (FP64 reference
+  // arithmetic), which would split this float polynomial into mul + add
+  float q = fmaf(s, -0.01172120f, 0.05265332f);
+  q = fmaf(s, q, -0.11643287f);
+  q = fmaf(s, q, 0.19354346f);
+  q = fmaf(s, q, -0.33262347f);
+  q = fmaf(s, q, 0.99997726f);
+  float r = a * q;
   if (ay > ax) r = 1.57079637f - r;
   if (x < 0.0f) r = 3.14159274f - r;
   return y < 0.0f ? -r : r;
