@@ -203,8 +203,14 @@ int ds_lidar_supported(void);
 void ds_struct_sizes(int64_t out[4]);
 const char *ds_last_error(void);
 
+/* Bind packed world tables + mutable state (device pointers, caller-owned)
+ * and a validated config to a handle: replaces SimBatch.__init__
+ * (engine.py:591-624) over the World.__init__ tables (engine.py:173-314).
+ * Rejects unknown dynamics / collision behaviour / sensor modes like
+ * SimConfig / ObsConfig (engine.py:59-67, observation.py:61-67). */
 int ds_create(const ds_tables *tables, const ds_config *cfg, ds_state *state,
               int device, ds_handle **out);
+/* SimBatch.close (engine.py:669-671); frees only the handle. */
 int ds_destroy(ds_handle *h);
 
 /* Reset the worlds whose world_mask[w] != 0 (device [n_worlds] u8; NULL = all)
@@ -214,6 +220,12 @@ int ds_reset(ds_handle *h, const uint8_t *world_mask, void *obs, float *rewards,
              uint8_t *dones, const float *obs_scale, int32_t *sel_idx,
              void *stream);
 
+/* SimBatch.step (engine.py:626-649): World.step (engine.py:357-498) of every
+ * world -- dynamics, replay, collisions, goal / removal / horizon -- then
+ * _fill_obs (engine.py:500-512); with auto_reset, VecDriveEnv.step's reset of
+ * finished worlds (env.py:95-124).  Two kernels on `stream`, no host sync.
+ * Row-count mismatches are the caller's ActionCountMismatch (engine.py:37-38,
+ * 629-631). */
 int ds_step(ds_handle *h, const ds_step_args *args, void *stream);
 
 /* Recompute observations from the current state only (World.observe). */
