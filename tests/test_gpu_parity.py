@@ -155,6 +155,14 @@ def test_lidar_c4_shape_parity():
     run_free(None, raw=raw, cfg=cfg, steps=12)
 
 
+def test_lidar_delta_local_remove_agent_parity():
+    """LiDAR with delta-local dynamics (3 action columns) and removal."""
+    cfg = SimConfig(init_mode="all_valid", dynamics="delta_local", collision_behavior="remove_agent",
+                    obs=ObsConfig(mode="lidar", n_rays=40, max_range=35.0))
+    raw = generate(WaymoSpec(n_worlds=4, n_agents=48, n_points=3000, seed=31))
+    run_free(None, raw=raw, cfg=cfg, steps=40)
+
+
 def test_view_cone_parity_with_head_rotation():
     cfg = SimConfig(init_mode="all_valid", collision_behavior="remove_agent",
                     obs=ObsConfig(mode="view_cone", n_rays=17, fov=2.5, max_range=70.0))
