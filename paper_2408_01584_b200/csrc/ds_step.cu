@@ -127,14 +127,21 @@ __device__ bool offroad_query(const ds_tables &T, const ds_config &C, int w, dou
   const int ix0 = cell_of(gx0, 0, nx - 1), ix1 = cell_of(gx1, 0, nx - 1);
   const int iy0 = cell_of(gy0, 0, ny - 1), iy1 = cell_of(gy1, 0, ny - 1);
   for (int iy = iy0; iy <= iy1; ++iy) {
-    for (int ix = ix0; ix <= ix1; ++ix) {
-      const int64_t cell = cbase + (int64_t)iy * nx + ix;
-      const int b = T.eseg_cell_start[cell], e = T.eseg_cell_start[cell + 1];
-      for (int k = b; k < e; ++k) {
-        const float4 q = erel[k];
-        if (fmaxf(q.x, q.z) < fcx - frx || fminf(q.x, q.z) > fcx + frx ||
-            fmaxf(q.y, q.w) < fcy - fry || fminf(q.y, q.w) > fcy + fry)
+    // the cells ix0..ix1 of one grid row are consecutive bins: one range
+    const int64_t crow = cbase + (int64_t)iy * nx;
+    const int b = T.eseg_cell_start[crow + ix0], e = T.eseg_cell_start[crow + ix1 + 1];
+    for (int k0 = b; k0 < e; k0 += 4) {
+      // four float prefilter loads in flight, then the tests
+      float4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        q[u] = k0 + u < e ? erel[k0 + u] : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (fmaxf(q[u].x, q[u].z) < fcx - frx || fminf(q[u].x, q[u].z) > fcx + frx ||
+            fmaxf(q[u].y, q[u].w) < fcy - fry || fminf(q[u].y, q[u].w) > fcy + fry)
           continue;
+        const int k = k0 + u;
         const double ax = T.eseg_ax[k], ay = T.eseg_ay[k], bx = T.eseg_bx[k], by = T.eseg_by[k];
         // segment AABB vs box AABB (with slack): a superset prefilter
         if (fmax(ax, bx) < cx - rx || fmin(ax, bx) > cx + rx || fmax(ay, by) < cy - ry ||
