@@ -233,7 +233,7 @@ __device__ __forceinline__ double ray_box(double ox, double oy, double dx, doubl
 }
 
 template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 2) obs_lidar_kernel(
+__global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 : 1)) obs_lidar_kernel(
     ds_tables T, ds_config C, ds_state St, const uint8_t *mask, const ObsOut O, const float *scale,
     int obs_width) {
   const int w = blockIdx.x;
