@@ -314,21 +314,6 @@ __device__ int select_serial(const Src &src, int k, double radius, float r2hi, c
   return cnt;
 }
 
-// Exact ascending top-min(n_valid, k) by (distance, id) given candidate keys
-// with |a - d^2| <= D.  Payloads land in S.sel_pl()[0..m).  Warp-collective.
-//  * rho: the radius the source currently covers (< radius when the caller
-//    narrowed it with a search hint, see hint_radius).  A narrowed pass 1 is
-//    used only if every bucket the selection touches provably lies inside
-//    the disc ((bmax + 1) w + D <= rho^2), else it reruns on the full radius.
-//    On return, bound_out holds a bound on the k-th distance (0 when fewer
-//    than k candidates exist).
-//  * ranking uses the float keys: two keys more than 2D apart are ordered
-//    exactly as the distances, so the exact FP64 hypot is evaluated only for
-//    near ties (|a_p - a_q| <= 2D) and possible out-of-radius keys.
-// Buffered: pass 1 keeps (key, payload) in shared memory (global-points path).
-__device__ __forceinline__ double sel_r2hi(double radius, double D) {
-  return (double)(float)((radius * radius + D) * (1.0 + 1e-7) + 1e-30);
-}
 
 // Radius that provably contains the k nearest candidates given a hint that
 // bounds the k-th distance (triangle inequality).  The narrowed selection
@@ -434,6 +419,18 @@ __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float be
   return n_valid < k ? n_valid : k;
 }
 
+// Exact ascending top-min(n_valid, k) by (distance, id) given candidate keys
+// with |a - d^2| <= D.  Payloads land in S.sel_pl()[0..m).  Warp-collective.
+//  * rho: the radius the source currently covers (< radius when the caller
+//    narrowed it with a search hint, see hint_radius).  A narrowed pass 1 is
+//    used only if every bucket the selection touches provably lies inside
+//    the disc ((bmax + 1) w + D <= rho^2), else it reruns on the full radius.
+//    On return, bound_out holds a bound on the k-th distance (0 when fewer
+//    than k candidates exist).
+//  * ranking uses the float keys: two keys more than 2D apart are ordered
+//    exactly as the distances, so the exact FP64 hypot is evaluated only for
+//    near ties (|a_p - a_q| <= 2D) and possible out-of-radius keys.
+// Buffered: pass 1 keeps (key, payload) in shared memory (global-points path).
 // Exact ascending top-min(n_valid, k) by (distance, id).  Direct: small
 // candidate sets (partners) are compacted straight into G and ranked as one
 // bucket; a larger set takes the histogram path.

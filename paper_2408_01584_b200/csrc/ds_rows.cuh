@@ -8,12 +8,6 @@ namespace ds {
 
 constexpr unsigned kFullMask = 0xffffffffu;
 
-__device__ __forceinline__ int clampi(double f, int lo, int hi) {
-  if (f < (double)lo) return lo;
-  if (f > (double)hi) return hi;
-  return (int)f;
-}
-
 __device__ __forceinline__ int clampf(float f, int lo, int hi) {
   if (f < (float)lo) return lo;
   if (f > (float)hi) return hi;
