@@ -23,7 +23,17 @@ struct StepShared {
   // circumcircle prefilter: float position relative to the world's grid
   // origin, circumradius padded by the float rounding bound (> 0: eligible)
   float4 *pre;
+  // sweep-and-prune order: left edges of the padded circles' x-intervals
+  // (+inf: not eligible) and agent ids, sorted ascending over sort_n slots
+  float *skey;
+  int *sord;
 };
+
+__host__ __device__ inline int pow2_at_least(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
 
 __device__ __forceinline__ StepShared carve_step(void *base, int amax) {
   StepShared sh;
@@ -39,11 +49,14 @@ __device__ __forceinline__ StepShared carve_step(void *base, int amax) {
   sh.hit = sh.elig + amax;
   sh.pre = reinterpret_cast<float4 *>(
       (reinterpret_cast<uintptr_t>(sh.hit + amax) + 15) & ~uintptr_t(15));
+  sh.skey = reinterpret_cast<float *>(sh.pre + amax);
+  sh.sord = reinterpret_cast<int *>(sh.skey + pow2_at_least(amax));
   return sh;
 }
 
 size_t step_smem_bytes(int max_agents) {
-  return (size_t)max_agents * (7 * sizeof(double) + 2) + 16 + (size_t)max_agents * sizeof(float4);
+  return (size_t)max_agents * (7 * sizeof(double) + 2) + 16 + (size_t)max_agents * sizeof(float4) +
+         (size_t)pow2_at_least(max_agents) * (sizeof(float) + sizeof(int));
 }
 
 // SAT over the 4 box axes, _fastpath.sat_pairs (fp:29-53); (i, j) with i < j.
@@ -317,27 +330,62 @@ __global__ void __launch_bounds__(MAXT, MINB) step_kernel(ds_tables T, ds_config
   __syncthreads();
 
   bool collided = false, offroad = false;
-  if (act_here && sh.elig[tid]) {
-    // every unordered pair once: agent i tests i + 1 .. i + A/2 (mod A) and
-    // flags both ends (SAT always runs on (min, max), so the result is the
-    // one either end would compute)
-    const float4 pi = sh.pre[tid];
-    const int half = A >> 1;
+  // Agent-agent pairs by sweep and prune: sort the padded circles' x-intervals
+  // by their left edge (bitonic, ties by id), then each sorted position scans
+  // forward only while the next left edge is inside its own interval -- every
+  // pair whose circles can overlap is tested exactly once, and both ends are
+  // flagged (SAT runs on (min, max) id, so either end computes the same bits).
+  const int sort_n = pow2_at_least(A);
+  for (int e = tid; e < sort_n; e += blockDim.x) {
+    float key = INFINITY;
+    if (e < A) {
+      const float4 pe = sh.pre[e];
+      if (pe.w != 0.0f) key = pe.x - pe.z;
+    }
+    sh.skey[e] = key;
+    sh.sord[e] = e;
+  }
+  __syncthreads();
+  for (int size = 2; size <= sort_n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int e = tid; e < sort_n; e += blockDim.x) {
+        const int o = e ^ stride;
+        if (o > e) {
+          const float ke = sh.skey[e], ko = sh.skey[o];
+          const int ie = sh.sord[e], io = sh.sord[o];
+          const bool greater = ke > ko || (ke == ko && ie > io);
+          if (greater == ((e & size) == 0)) {
+            sh.skey[e] = ko;
+            sh.skey[o] = ke;
+            sh.sord[e] = io;
+            sh.sord[o] = ie;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int p = tid; p < A; p += blockDim.x) {
+    const float kp = sh.skey[p];
+    if (kp == INFINITY) continue;          // not eligible (sorted last)
+    const int i = sh.sord[p];
+    const float4 pi = sh.pre[i];
+    const float right = pi.x + pi.z + 1e-4f * (1.0f + fabsf(pi.x));
     bool hit_any = false;
-    for (int d = 1; d <= half; ++d) {
-      int j = tid + d;
-      if (j >= A) j -= A;
+    for (int q = p + 1; q < A; ++q) {
+      if (sh.skey[q] > right) break;       // this and all later intervals start beyond i's
+      const int j = sh.sord[q];
       // boxes lie inside their circumcircles: disjoint circles cannot collide
       // (float superset test on padded radii; SAT below decides exactly)
       const float4 pj = sh.pre[j];
       const float dx = pj.x - pi.x, dy = pj.y - pi.y, rr = pi.z + pj.z;
-      if (pj.w == 0.0f || fmaf(dx, dx, dy * dy) > rr * rr * (1.0f + 1e-5f)) continue;
-      if (j > tid ? sat_hit(sh, tid, j) : sat_hit(sh, j, tid)) {
+      if (fmaf(dx, dx, dy * dy) > rr * rr * (1.0f + 1e-5f)) continue;
+      if (j > i ? sat_hit(sh, i, j) : sat_hit(sh, j, i)) {
         hit_any = true;
         sh.hit[j] = 1;
       }
     }
-    if (hit_any) sh.hit[tid] = 1;
+    if (hit_any) sh.hit[i] = 1;
   }
   __syncthreads();
   if (act_here && sh.elig[tid]) {
