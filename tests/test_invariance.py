@@ -75,3 +75,22 @@ def test_grid_cell_size_does_not_change_results(mode, cells):
         for (o, r, d, i), (bo, br, bd, bi) in zip(outs, base):
             assert np.array_equal(o, bo), f"cell {cs}: observations differ"
             assert np.array_equal(r, br) and np.array_equal(d, bd) and np.array_equal(i, bi)
+
+
+def test_full_circle_view_cone_equals_lidar():
+    """A view cone with fov = 2 pi and no head rotation is the LiDAR sweep
+    (observation.py:213-220; T/test_observation.py:243-250)."""
+    import math
+    raw = generate(WaymoSpec(n_worlds=3, n_agents=40, n_points=3000, seed=13))
+    outs = []
+    for obs in (ObsConfig(mode="lidar", n_rays=36, max_range=40.0),
+                ObsConfig(mode="view_cone", n_rays=36, fov=2 * math.pi, max_range=40.0)):
+        cfg = SimConfig(init_mode="all_valid", collision_behavior="remove_agent", obs=obs)
+        b = SimBatch.from_raw(raw, cfg, device="cuda:0")
+        rng = np.random.default_rng(4)
+        acts = [actions_for(cfg, b.n_controlled, rng).astype(np.float32) for _ in range(15)]
+        outs.append(_run(b, acts))
+        b.close()
+    for (o1, r1, d1, i1), (o2, r2, d2, i2) in zip(*outs):
+        assert np.array_equal(o1, o2)
+        assert np.array_equal(r1, r2) and np.array_equal(d1, d2) and np.array_equal(i1, i2)
