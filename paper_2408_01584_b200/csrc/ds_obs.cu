@@ -109,8 +109,10 @@ __host__ __device__ inline WarpLayout warp_layout(const ds_config &c, bool buffe
 }
 
 // per agent: x, y, heading, speed, length, width, cos, sin (f64) + visible (u8)
+// + per row: the agent's local index and flags (row loop header from shared)
 __host__ __device__ inline size_t agents_bytes(int max_agents) {
-  return al16((size_t)max_agents * (8 * sizeof(double) + 1));
+  return al16((size_t)max_agents * (8 * sizeof(double) + 1)) +
+         al16((size_t)max_agents * (sizeof(uint16_t) + sizeof(uint16_t)));
 }
 
 size_t obs_smem_bytes_shared(const ds_config &cfg, int max_agents, int max_points, int warps) {
@@ -682,6 +684,15 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     const uint16_t f = St.flags[g];
     avis[i] = (f & DS_F_PRESENT) && !(f & DS_F_REMOVED);
   }
+  // row -> (local agent, flags), so the row loop starts from shared memory
+  uint16_t *rloc = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(ax) +
+                                                al16((size_t)amax * (8 * sizeof(double) + 1)));
+  uint16_t *rflg = rloc + amax;
+  for (int r = threadIdx.x; r < nrow; r += blockDim.x) {
+    const int64_t g = T.row_agent[c0 + r];
+    rloc[r] = (uint16_t)(g - a0);
+    rflg[r] = St.flags[g];
+  }
   if (SharedPts) {
     const float2 *src = reinterpret_cast<const float2 *>(T.gpt_xy) + p0;
     for (int j = threadIdx.x; j < np; j += blockDim.x) pts[j] = src[j];
@@ -701,9 +712,9 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
 
   for (int r = warp; r < nrow; r += WARPS) {
     const int64_t orow = c0 + r;
-    const int64_t g = T.row_agent[orow];
-    const int i = (int)(g - a0);
-    const uint16_t f = St.flags[g];
+    const int i = rloc[r];
+    const int64_t g = a0 + i;
+    const uint16_t f = rflg[r];
     if (f & (DS_F_DONE | DS_F_REMOVED)) {
       // finished / removed rows are zero-filled (engine.py:502-512)
       zero_row(O, orow, lane);
