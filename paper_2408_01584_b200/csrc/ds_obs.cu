@@ -11,7 +11,7 @@
 //
 // Exact top-k (the reference's insertion sort = ascending (distance, index)):
 //  pass 1  every candidate gets a cheap float key a ~ d^2 with a proven
-//          absolute error bound D; a 256-bucket histogram of a over
+//          absolute error bound D; a 128-bucket histogram of a over
 //          [0, r^2 + D] gives the threshold bucket b* (first bucket whose
 //          cumulative count reaches k);
 //  pass 2  candidates in buckets <= b*+1 are counting-sort scattered into a
@@ -32,7 +32,7 @@
 namespace ds {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kNB = 256;       // histogram buckets
+constexpr int kNB = 128;       // histogram buckets
 constexpr int kCandGlobal = 640;  // buffered pass-1 candidates (global-points variant)
 constexpr int kCandShared = 224;  // (shared-points variant: hint-narrowed scans)
 // warps per world CTA: as many as the shared memory allows (occupancy is what
@@ -519,11 +519,12 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
   uint32_t total, n_g, incl, local;
   uint32_t cnt[kPer];
   int bstar, bmax, nbuf;
-  static_assert(kPer == 8, "the histogram is read / written as two uint4 per lane");
+  static_assert(kPer % 4 == 0, "the histogram is read / written as uint4 per lane");
+  constexpr int kVec = kPer / 4;
   uint4 *const hc4 = reinterpret_cast<uint4 *>(S.hc());
   while (true) {
-    hc4[lane] = make_uint4(0u, 0u, 0u, 0u);
-    hc4[lane + 32] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int v = 0; v < kVec; ++v) hc4[lane + 32 * v] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
     nbuf = 0;
     src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
@@ -538,9 +539,11 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     });
     __syncwarp();
     {
-      const uint4 c0 = hc4[2 * lane], c1 = hc4[2 * lane + 1];
-      cnt[0] = c0.x; cnt[1] = c0.y; cnt[2] = c0.z; cnt[3] = c0.w;
-      cnt[4] = c1.x; cnt[5] = c1.y; cnt[6] = c1.z; cnt[7] = c1.w;
+#pragma unroll
+      for (int v = 0; v < kVec; ++v) {
+        const uint4 c = hc4[kVec * lane + v];
+        cnt[4 * v] = c.x; cnt[4 * v + 1] = c.y; cnt[4 * v + 2] = c.z; cnt[4 * v + 3] = c.w;
+      }
     }
     local = 0;
 #pragma unroll
@@ -584,8 +587,9 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     hv[q] = (run2 << 16) | cnt[q];
     run2 += cnt[q];
   }
-  hc4[2 * lane] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
-  hc4[2 * lane + 1] = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+#pragma unroll
+  for (int v = 0; v < kVec; ++v)
+    hc4[kVec * lane + v] = make_uint4(hv[4 * v], hv[4 * v + 1], hv[4 * v + 2], hv[4 * v + 3]);
   __syncwarp();
   {
     const uint32_t hb = S.hc()[bmax];   // (start << 16) | count of the last kept bucket
