@@ -11,8 +11,13 @@ in-loop torch policy (the reference trainer's ActorCritic, ippo.py:48-66, in
 bf16 on bf16 observations) and the fused device sampler choosing the
 discrete actions.  Metric: agent-steps/s (ASPS = CASPS,
 init_mode="all_valid"), whole job = sum over ranks.  Worlds shard across ranks
-with no collective on the step path ("scaling": "weak": each rank owns the
-configured world count; scene seed = global world id).  The working set (C3:
+with no collective on the step path (scene seed = global world id): at N = 1
+the config's worlds; at N > 1 the main line is STRONG scaling (the config's
+worlds split into contiguous shards) plus a "weak" sub-object (the config's
+worlds on every rank), BASELINE.md §3.4.  `--gpus N` outside torchrun
+launches the N ranks itself.  Rank 0 at N = 1 also steps one full episode of
+the benched batch against the C oracle on the host cores: the line's
+"parity" verdict and its "cpu_baseline".  The working set (C3:
 1.7 GB of observations written per step, 0.7 GB of road tables) exceeds the
 126 MB L2, so no flush is needed between steps.
 """
@@ -169,14 +174,13 @@ def sim_config(name):
 
 class CpuSample:
     """The C oracle (restatement of the reference, bit-exact with it on the
-    golden fixtures) stepping a bounded sample of the same workload on the
-    host cores (OpenMP over worlds).  For c5 the reference trainer's policy
-    runs on the CPU too."""
+    golden fixtures; its own table builder, no product code) stepping a
+    bounded sample of the same workload on the host cores (OpenMP over
+    worlds).  For c5 the reference trainer's policy runs on the CPU too."""
 
     def __init__(self, name: str, threads: int):
         import numpy as np
         from oracle.oracle import OracleBatch, build
-        from paper_2408_01584_b200.packing import pack
         from paper_2408_01584_b200.synthetic import WaymoSpec, generate
         build()
         W, A, P = CONFIGS[name][:3]
@@ -184,7 +188,7 @@ class CpuSample:
         self.cfg = sim_config(name)
         ws = min(CPU_WORLDS[name], W)
         raw = generate(WaymoSpec(n_worlds=ws, n_agents=A, n_points=P, seed=0))
-        self.ora = OracleBatch(pack(raw, self.cfg), self.cfg, n_threads=threads)
+        self.ora = OracleBatch(raw, self.cfg, n_threads=threads)
         self.agents = int(self.ora.pw.n_instantiated.sum())
         self.rng = np.random.default_rng(0)
         self.desc = f"{ws} worlds x {A} agents"
@@ -234,8 +238,20 @@ class CpuSample:
         return self.agents * k / el, f"{self.desc} x {k} steps ({el:.1f} s)"
 
 
-def bench_config(name: str, W: int, W_total: int, world: int,
-                 l2: str = "working set > L2 (no flush needed)") -> dict:
+def leg_worlds(args, world: int, rank: int):
+    """(worlds on this rank, global id of its first world, worlds in the job)
+    of the main line: N = 1 the config's worlds; N > 1 STRONG scaling, the
+    config's worlds split into contiguous shards."""
+    total = args.worlds or CONFIGS[args.config][0]
+    if world == 1:
+        return total, 0, total
+    import numpy as np
+    from paper_2408_01584_b200.parallel import shard_ranges
+    lo, hi = shard_ranges(np.ones(total), world)[rank]
+    return hi - lo, lo, total
+
+
+def bench_config(name: str, W: int, W_total: int, world: int, scaling: str) -> dict:
     """The `config` object of a bench line (both arms print the same one)."""
     from paper_2408_01584_b200.config import obs_width
     _, A, P, dyn, coll, okw, workload = CONFIGS[name]
@@ -243,8 +259,8 @@ def bench_config(name: str, W: int, W_total: int, world: int,
     return {"workload": workload, "worlds_per_gpu": W, "worlds_total": W_total,
             "agents": A, "road_points": P, "dynamics": dyn, "collision": coll,
             "obs_mode": cfg.obs.mode, "obs_width": obs_width(cfg.obs), "episode_steps": 91,
-            "auto_reset": True, "l2": l2,
-            "parallelism": f"world shards x {world} GPU (no step collective)"}
+            "auto_reset": True,
+            "parallelism": f"world shards x {world} GPU (no step collective), {scaling} scaling"}
 
 
 def run_reference(args, rank):
@@ -255,17 +271,14 @@ def run_reference(args, rank):
     threads = os.cpu_count() or 1
     cs = CpuSample(args.config, threads)
     value, sample = cs.rate(args.steps, warmup=args.warmup, budget_s=120.0)
-    W = args.worlds or CONFIGS[args.config][0]
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    W_total = W if args.strong else W * world
-    if args.strong:
-        W = -(-W // world)
+    world = args.gpus
+    W, _, W_total = leg_worlds(args, world, 0)
+    scaling = "strong" if world > 1 else "weak"
     line = {"impl": "reference", "metric": "agent_steps_per_sec", "value": value,
             "unit": "agent-steps/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "strong" if args.strong else "weak",
+            "warmup": args.warmup, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": bench_config(args.config, W, W_total, world),
+            "config": bench_config(args.config, W, W_total, world, scaling),
             "cpu_baseline": {"value": value, "unit": "agent-steps/s", "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "agent-steps/s", "h2d_bytes_per_step": 0,
@@ -273,111 +286,144 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
-    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--worlds", type=int, default=None, help="override worlds per GPU")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--strong", action="store_true",
-                    help="strong scaling: the config's worlds split over the ranks "
-                         "(default weak: the config's worlds on every rank)")
-    args = ap.parse_args()
+def parity_check(batch, raw, cfg, dev, n_worlds: int, steps: int, threads: int) -> tuple:
+    """The bench's own parity verdict and CPU baseline in one pass: a full
+    episode of the benched batch (reset, `steps` steps of the bench's device
+    actions, no auto-reset) against the C oracle stepping the first
+    `n_worlds` worlds with the same actions on the host cores.  Flags
+    (rewards, dones, goal / collision / off-road) and the partner / road-point
+    selection indices must be bit-exact, float32 observations within
+    2 ulp + 1e-6 of the FP64 oracle, FP64 poses within 1e-9 m / 1e-12 rad.
+    Returns (parity dict, cpu_baseline dict)."""
+    import numpy as np
+    import torch
+    from oracle.oracle import OracleBatch, build
+    from paper_2408_01584_b200.engine import random_actions
+    build()
+    nw = min(n_worlds, batch.n_worlds)
+    ora = OracleBatch(raw.subset(range(nw)), cfg, n_threads=threads)
+    rows = int(batch.offsets[nw])
+    n_ag = int(batch.packed.a_off[nw])
+    if ora.pw.n_controlled != rows or ora.pw.n_agents != n_ag:
+        raise RuntimeError("oracle and batch disagree on the controlled rows")
+    radial = cfg.obs.mode == "radial"
+    sel_w = cfg.obs.max_agents_obs + cfg.obs.max_road_points_obs
+    sel = torch.full((batch.n_controlled, sel_w), -7, dtype=torch.int32, device=dev) if radial else None
+    batch.reset(sel_idx=sel)
+    res = {"worlds": nw, "rows": rows, "steps": steps, "flag_mismatches": 0, "sel_mismatches": 0,
+           "obs_out_of_tol": 0, "max_obs_err": 0.0,
+           "tolerance": "flags/indices bit-exact; obs 2 f32 ulp + 1e-6; poses 1e-9 m, 1e-12 rad"}
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        run_reference(args, rank)
-        return
+    def compare(o_obs, o_rew, o_done, o_info):
+        got = batch.observations[:rows].cpu().numpy().astype(np.float64)
+        ref = o_obs.astype(np.float32)
+        err = np.abs(got - ref.astype(np.float64))
+        tol = 2.0 * np.spacing(np.abs(ref)).astype(np.float64) + 1e-6
+        res["obs_out_of_tol"] += int((err > tol).sum())
+        res["max_obs_err"] = max(res["max_obs_err"], float(err.max()) if err.size else 0.0)
+        bad = (batch.rewards[:rows].cpu().numpy() != o_rew.astype(np.float32)) | \
+              (batch.dones[:rows].cpu().numpy() != o_done)
+        info = batch._info[:, :rows].cpu().numpy()
+        for k, key in enumerate(("goal", "veh_collision", "offroad")):
+            bad |= info[k] != o_info[key]
+        res["flag_mismatches"] += int(bad.sum())
+        if radial:
+            res["sel_mismatches"] += int((sel[:rows].cpu().numpy() != ora.sel_idx[:rows]).any(1).sum())
 
+    zeros = {k: np.zeros(rows, bool) for k in ("goal", "veh_collision", "offroad")}
+    compare(ora.observations, np.zeros(rows), np.zeros(rows, bool), zeros)
+    cpu_s = 0.0
+    for t in range(1, steps + 1):
+        act = random_actions(batch.n_controlled, cfg, 0, t, dev)
+        batch.step(act, sel_idx=sel)
+        a_h = act[:rows].cpu().numpy().astype(np.float64)
+        t0 = time.perf_counter()
+        o = ora.step(a_h)
+        cpu_s += time.perf_counter() - t0
+        compare(*o)
+    x, y, h = (v[:n_ag].cpu().numpy() for v in (batch._x, batch._y, batch._h))
+    res["max_pose_err_m"] = float(max(np.abs(x - ora.x[:n_ag]).max(), np.abs(y - ora.y[:n_ag]).max()))
+    dh = np.abs(np.mod(h - ora.heading[:n_ag] + np.pi, 2 * np.pi) - np.pi)
+    res["max_heading_err_rad"] = float(dh.max())
+    res["state_flag_mismatches"] = int((batch._flags[:n_ag].cpu().numpy().astype(np.uint16)
+                                        != ora.flags[:n_ag]).sum())
+    res["ok"] = (res["flag_mismatches"] == 0 and res["sel_mismatches"] == 0
+                 and res["obs_out_of_tol"] == 0 and res["state_flag_mismatches"] == 0
+                 and res["max_pose_err_m"] <= 1e-9 and res["max_heading_err_rad"] <= 1e-12)
+    agents = int(ora.pw.n_instantiated.sum())
+    cpu = {"value": agents * steps / cpu_s, "unit": "agent-steps/s", "cores": threads,
+           "kind": "port", "sample": f"the parity episode: {nw} worlds x {agents // max(nw, 1)} agents "
+                                     f"x {steps} steps ({cpu_s:.1f} s)"}
+    return res, cpu
+
+
+class Leg:
+    """One benched batch (a rank's shard) and its step function."""
+
+    def __init__(self, args, W: int, w_off: int, rank: int, dev):
+        import torch
+        from paper_2408_01584_b200.config import obs_width
+        from paper_2408_01584_b200.engine import SimBatch, random_actions
+        from paper_2408_01584_b200.synthetic import WaymoSpec, generate
+        _, A, P, dyn, coll, okw, workload = CONFIGS[args.config]
+        self.cfg = cfg = sim_config(args.config)
+        self.width = obs_width(cfg.obs)
+        self.P, self.A, self.W = P, A, W
+        self.dev = dev
+        t0 = time.perf_counter()
+        self.raw = generate(WaymoSpec(n_worlds=W, n_agents=A, n_points=P, seed=0, world_offset=w_off))
+        self.rl = args.config == "c5"
+        if self.rl:
+            from paper_2408_01584_b200.env import EnvConfig, VecDriveEnv
+            from paper_2408_01584_b200.policy import ActorCritic
+            # rollout formats: bf16 observations in rows padded to 8 (the policy
+            # GEMM's input, no cast), a bf16 policy with 16-B aligned operands,
+            # one fused sampler launch per step
+            self.env = VecDriveEnv(EnvConfig(raw=self.raw, sim=cfg, device=str(dev),
+                                             obs_dtype="bfloat16"))
+            self.batch = self.env.batch
+            self.policy = ActorCritic(self.width, self.env.n_actions, pad_to=8).to(dev).to(torch.bfloat16)
+            self.obs = self.env.reset()
+        else:
+            self.batch = SimBatch.from_raw(self.raw, cfg, device=dev)
+            self.acts = [random_actions(self.batch.n_controlled, cfg, 0, t, dev) for t in range(8)]
+        self.setup_s = time.perf_counter() - t0
+        self.rank = rank
+
+    def step(self, t, events=None):
+        import torch
+        if self.rl:
+            from paper_2408_01584_b200.engine import sample_categorical
+            with torch.inference_mode():
+                logits, value = self.policy(self.obs)
+                idx = sample_categorical(logits, seed=1234 + self.rank, counter=t)
+            obs, rew, done, infos = self.env.step(idx)
+            self.obs = obs
+            return rew
+        return self.batch.step(self.acts[t % 8], auto_reset=True, events=events).rewards
+
+    def restart(self):
+        """Every timed leg covers the same episode phase (steps W .. W+K after
+        a reset): work per step changes over an episode (remove_agent)."""
+        import torch
+        if self.rl:
+            self.obs = self.env.reset()
+        else:
+            self.batch.reset()
+        torch.cuda.synchronize(self.dev)
+
+
+def time_leg(leg: Leg, args, world: int, barrier, local_rank: int) -> dict:
+    """Device-timed steps (inputs resident in HBM), the per-kernel split and
+    the end-to-end leg through the public API with host buffers."""
     import torch
     import torch.distributed as dist
-    from paper_2408_01584_b200.config import obs_width
-    from paper_2408_01584_b200.engine import SimBatch, random_actions
-    from paper_2408_01584_b200.synthetic import WaymoSpec, generate
-
-    # DS_BENCH_SHARE_GPU=1 (test only): ranks share the visible GPUs over gloo,
-    # to exercise the N > 1 path on a one-GPU box; never used for bench lines
-    share = os.environ.get("DS_BENCH_SHARE_GPU") == "1"
-    gpu = local_rank % torch.cuda.device_count() if share else local_rank
-    torch.cuda.set_device(gpu)
-    dev = torch.device("cuda", gpu)
-    if world > 1:
-        if share:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
-    W, A, P, dyn, coll, okw, workload = CONFIGS[args.config]
-    if args.worlds:
-        W = args.worlds
-    W_total = W * world
-    w_off = rank * W
-    if args.strong:
-        import numpy as np
-        from paper_2408_01584_b200.parallel import shard_ranges
-        W_total = W
-        lo, hi = shard_ranges(np.ones(W), world)[rank]
-        W, w_off = hi - lo, lo
-    cfg = sim_config(args.config)
-    width = obs_width(cfg.obs)
-    t_setup = time.perf_counter()
-    raw = generate(WaymoSpec(n_worlds=W, n_agents=A, n_points=P, seed=0, world_offset=w_off))
-    rl = args.config == "c5"
-    if rl:
-        from paper_2408_01584_b200.engine import sample_categorical
-        from paper_2408_01584_b200.env import EnvConfig, VecDriveEnv
-        from paper_2408_01584_b200.policy import ActorCritic
-        # rollout formats: bf16 observations in rows padded to 8 (the policy
-        # GEMM's input, no cast), a bf16 policy with 16-B aligned operands,
-        # one fused sampler launch per step
-        env = VecDriveEnv(EnvConfig(raw=raw, sim=cfg, device=str(dev), obs_dtype="bfloat16"))
-        batch = env.batch
-        policy = ActorCritic(width, env.n_actions, pad_to=8).to(dev).to(torch.bfloat16)
-        obs0 = env.reset()
-    else:
-        batch = SimBatch.from_raw(raw, cfg, device=dev)
-        acts = [random_actions(batch.n_controlled, cfg, 0, t, dev) for t in range(8)]
-    t_setup = time.perf_counter() - t_setup
-    n = batch.n_controlled
+    dev = leg.dev
     stream = torch.cuda.current_stream(dev)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    state = {"obs": obs0} if rl else {}
-
-    def one_step(t, events=None):
-        if rl:
-            with torch.inference_mode():
-                logits, value = policy(state["obs"])
-                idx = sample_categorical(logits, seed=1234 + rank, counter=t)
-            obs, rew, done, infos = env.step(idx)
-            state["obs"] = obs
-            return rew
-        return batch.step(acts[t % 8], auto_reset=True, events=events).rewards
-
-    def restart():
-        # every timed leg covers the same episode phase (steps W .. W+K after
-        # a reset): work per step changes over an episode (remove_agent)
-        if rl:
-            state["obs"] = env.reset()
-        else:
-            batch.reset()
-        torch.cuda.synchronize(dev)
-
-    restart()
+    leg.restart()
     for t in range(args.warmup):
-        one_step(t)
+        leg.step(t)
     torch.cuda.synchronize(dev)
-
-    # ---- device-resident timed region (inputs already in HBM); the
-    # per-kernel split comes from a separate pass after it (no event records
-    # inside the timed steps)
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     # small working sets (C1, C2 at a few worlds) would stay L2-resident across
@@ -401,7 +447,7 @@ def main():
         if flush_l2:
             flush_buf.fill_(float(t))
             step_ev[t][0].record(stream)
-        one_step(t)
+        leg.step(t)
         if flush_l2:
             step_ev[t][1].record(stream)
     end.record(stream)
@@ -412,7 +458,7 @@ def main():
     if flush_l2:
         ms = sum(a.elapsed_time(b) for a, b in step_ev)
     kernel_ms = None
-    if not rl:
+    if not leg.rl:
         # per-kernel split (CUDA events on the launching stream around each
         # kernel) over a further pass of the same steps, L2 flushed likewise
         n_ev = min(args.steps, 10)
@@ -420,13 +466,13 @@ def main():
         for e3 in ev:           # materialise the CUDA events (ds_step records raw handles)
             for e in e3:
                 e.record(stream)
-        restart()
+        leg.restart()
         for t in range(args.warmup):
-            one_step(t)
+            leg.step(t)
         for t in range(n_ev):
             if flush_l2:
                 flush_buf.fill_(float(t))
-            one_step(t, events=ev[t])
+            leg.step(t, events=ev[t])
         torch.cuda.synchronize(dev)
         kernel_ms = {"step_kernel": sum(e[0].elapsed_time(e[1]) for e in ev) / n_ev,
                      "obs_kernel": sum(e[1].elapsed_time(e[2]) for e in ev) / n_ev}
@@ -435,7 +481,7 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     # units all ranks processed: every rank's agents (allreduce of the counts)
-    agents_total = batch.total_agents
+    agents_total = leg.batch.total_agents
     if world > 1:
         ta = torch.tensor([float(agents_total)], device=dev)
         dist.all_reduce(ta)
@@ -447,22 +493,23 @@ def main():
     # back (c1-c4: actions in, rewards/dones/info out through HostStepper,
     # whose copies overlap the kernels; c5: the policy samples the actions on
     # the device, the step's reward sum comes back).
-    if rl:
+    if leg.rl:
         rsum_h = torch.empty(1, dtype=torch.float32).pin_memory()
         h2d, d2h = 0, 4
     else:
         from paper_2408_01584_b200.engine import HostStepper
-        stepper = HostStepper(batch, act_dim=acts[0].shape[1])
-        host_acts = [a.cpu().pin_memory() for a in acts]
+        stepper = HostStepper(leg.batch, act_dim=leg.acts[0].shape[1])
+        host_acts = [a.cpu().pin_memory() for a in leg.acts]
         h2d, d2h = stepper.h2d_bytes_per_step, stepper.d2h_bytes_per_step
+
     def e2e_step(t):
-        if rl:
-            rew = one_step(t)
+        if leg.rl:
+            rew = leg.step(t)
             rsum_h.copy_(rew.sum().reshape(1), non_blocking=True)
         else:
             stepper.step(host_acts[t % 8])
 
-    restart()
+    leg.restart()
     for t in range(args.warmup):          # untimed warm-up of this leg's own ops
         e2e_step(t)
     barrier()
@@ -470,11 +517,11 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    if not rl:
+    if not leg.rl:
         stepper._h2d.wait_event(e0)        # the first action copy is inside the region
     for t in range(args.steps):
         e2e_step(t)
-    if not rl:
+    if not leg.rl:
         stream.wait_stream(stepper._d2h)   # the last result copy is inside the region
     e1.record(stream)
     torch.cuda.synchronize(dev)
@@ -484,70 +531,185 @@ def main():
         tt = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    e2e_value = agents_total * args.steps / (e2e_ms / 1e3)
+    return {"value": value, "ms": ms, "kernel_ms": kernel_ms, "clocks": clocks, "l2": l2_note,
+            "agents_total": agents_total,
+            "e2e": {"value": agents_total * args.steps / (e2e_ms / 1e3), "unit": "agent-steps/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}}
+
+
+def self_launch(args) -> int:
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one process per
+    GPU) with torch.distributed.run on 127.0.0.1 and return their exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def launch_check(world: int, rank: int):
+    """--launch-check: each rank joins a gloo group and rank 0 prints how
+    many ranks answered (the CPU test of the self-launch path)."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.ones(1)
+    if world > 1:
+        dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "world_size": world, "ranks_answered": int(t.item())}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--worlds", type=int, default=None,
+                    help="override the config's world count (N > 1: the total for strong "
+                         "scaling, per GPU for the weak sub-line)")
+    ap.add_argument("--no-cpu-baseline", action="store_true",
+                    help="skip the parity episode against the oracle (and its CPU timing)")
+    ap.add_argument("--no-weak", action="store_true", help="N > 1: skip the weak-scaling sub-line")
+    ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    if args.launch_check:
+        launch_check(world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    # DS_BENCH_SHARE_GPU=1 (test only): ranks share the visible GPUs over gloo,
+    # to exercise the N > 1 path on a one-GPU box; never used for bench lines
+    share = os.environ.get("DS_BENCH_SHARE_GPU") == "1"
+    gpu = local_rank % torch.cuda.device_count() if share else local_rank
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    if world > 1:
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    W, w_off, W_total = leg_worlds(args, world, rank)
+    scaling = "strong" if world > 1 else "weak"
+    leg = Leg(args, W, w_off, rank, dev)
+    main_leg = time_leg(leg, args, world, barrier, local_rank)
+    cfg, width, P, A = leg.cfg, leg.width, leg.P, leg.A
 
     # ---- episode statistics: the only collective, off the step path
     from paper_2408_01584_b200.parallel import allreduce_episode_stats, episode_stats
-    stats = allreduce_episode_stats(episode_stats(batch.episode_infos), device=dev)
+    stats = allreduce_episode_stats(episode_stats(leg.batch.episode_infos), device=dev)
 
     # ---- roofline of the dominant kernel (the observation kernel)
     peak, peak_kind = load_peaks()
-    act_dim = 1 if rl else acts[0].shape[1]
+    act_dim = 1 if leg.rl else leg.acts[0].shape[1]
     bpa = bytes_per_agent_step(act_dim, width, P, A)
     fl = radial_flops(P, A) if cfg.obs.mode == "radial" else \
-        lidar_flops(batch.packed, cfg.obs.max_range, cfg.obs.n_rays)
+        lidar_flops(leg.batch.packed, cfg.obs.max_range, cfg.obs.n_rays)
     hbm_bound = peak * 1e9 / bpa["total"]
     fp32_bound = 74.4e12 / fl
     roofline = None
+    kernel_ms = main_leg["kernel_ms"]
     if kernel_ms is not None:
-        achieved = bpa["obs_kernel"] * batch.n_controlled / (kernel_ms["obs_kernel"] / 1e3) / 1e9
+        n = leg.batch.n_controlled
+        achieved = bpa["obs_kernel"] * n / (kernel_ms["obs_kernel"] / 1e3) / 1e9
         kname = "obs_radial_kernel" if cfg.obs.mode == "radial" else "obs_lidar_kernel"
-        tr = load_traffic(args.config, kname) if (args.worlds or W) == CONFIGS[args.config][0] else None
+        tr = load_traffic(args.config, kname) if (W == CONFIGS[args.config][0]) else None
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": tr / 1e9 if tr else None,
                     "traffic_unit": "GB per launch (ncu dram__bytes_read+write)",
-                    "algorithmic_gb_per_launch": bpa["obs_kernel"] * batch.n_controlled / 1e9,
+                    "algorithmic_gb_per_launch": bpa["obs_kernel"] * n / 1e9,
                     "kernel": kname,
                     "bytes_per_agent_step": bpa["obs_kernel"], "peak_kind": peak_kind}
-    if rank == 0:
-        cpu = None
-        # the CPU baseline leg runs at N = 1 only (rank 0); N > 1 lines reuse it
-        if not args.no_cpu_baseline and world == 1:
-            threads = os.cpu_count() or 1
-            try:
-                v, sample = CpuSample(args.config, threads).rate(91, warmup=1, budget_s=20.0,
-                                                                  min_s=10.0)
-                cpu = {"value": v, "unit": "agent-steps/s", "cores": threads, "kind": "port",
+
+    # ---- parity episode against the oracle (rank 0, N = 1): the line's
+    # parity verdict and its CPU baseline
+    parity, cpu = None, None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        try:
+            if leg.rl:
+                cpu_v, sample = CpuSample(args.config, threads).rate(91, warmup=1, budget_s=20.0,
+                                                                     min_s=10.0)
+                cpu = {"value": cpu_v, "unit": "agent-steps/s", "cores": threads, "kind": "port",
                        "sample": sample}
-            except Exception as exc:   # report, never fake
-                cpu = {"value": None, "unit": "agent-steps/s", "cores": threads, "kind": "port",
-                       "sample": f"failed: {exc!r}"}
+                parity = {"skipped": "c5 steps the same simulator as c3 (policy-chosen actions); "
+                                     "parity is checked on the c1-c4 lines"}
+            else:
+                parity, cpu = parity_check(leg.batch, leg.raw, cfg, dev, CPU_WORLDS[args.config],
+                                           91, threads)
+        except Exception as exc:   # report, never fake
+            cpu = {"value": None, "unit": "agent-steps/s", "cores": threads, "kind": "port",
+                   "sample": f"failed: {exc!r}"}
+            parity = {"ok": False, "error": repr(exc)}
+
+    # ---- N > 1: the weak-scaling sub-line (the config's worlds on EVERY rank)
+    weak = None
+    if world > 1 and not args.no_weak:
+        Ww = args.worlds or CONFIGS[args.config][0]
+        leg.batch.close()
+        wleg = Leg(args, Ww, rank * Ww, rank, dev)
+        r = time_leg(wleg, args, world, barrier, local_rank)
+        weak = {"value": r["value"], "ms_per_step": r["ms"] / args.steps, "scaling": "weak",
+                "worlds_per_gpu": Ww, "worlds_total": Ww * world, "e2e": r["e2e"],
+                "kernel_ms": r["kernel_ms"], "clocks": r["clocks"]}
+        wleg.batch.close()
+    if rank == 0:
         total = max(int(stats[1]), 1)
         result = {
-            "metric": "agent_steps_per_sec", "value": value, "unit": "agent-steps/s",
+            "metric": "agent_steps_per_sec", "value": main_leg["value"], "unit": "agent-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if args.strong else "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": bench_config(args.config, W, W_total, world, l2_note),
-            "e2e": {"value": e2e_value, "unit": "agent-steps/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
-            "gpu_launches": (2 * args.steps) if not rl else 3 * args.steps,
+            "ms_per_step": main_leg["ms"] / args.steps, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": bench_config(args.config, W, W_total, world, scaling),
+            "l2": main_leg["l2"],
+            "e2e": main_leg["e2e"],
+            "gpu_launches": (2 * args.steps) if not leg.rl else 3 * args.steps,
             "roofline": roofline,
             "step_roofline": {"bytes_per_agent_step": bpa["total"],
                               "fp32_flop_per_agent_step": fl, "hbm_bound_asps": hbm_bound,
                               "fp32_bound_asps": fp32_bound,
                               "bound_asps": min(hbm_bound, fp32_bound),
-                              "frac": (value / world) / min(hbm_bound, fp32_bound)},
+                              "frac": (main_leg["value"] / world) / min(hbm_bound, fp32_bound)},
             "kernel_ms": kernel_ms,
-            "clocks": clocks,
+            "clocks": main_leg["clocks"],
             "cpu_baseline": cpu,
+            "parity": parity,
+            "weak": weak,
             "episodes": {"count": int(stats[0]), "goal_rate": stats[2] / total,
                          "veh_collision_rate": stats[3] / total, "offroad_rate": stats[4] / total},
-            "setup_s": t_setup,
+            "setup_s": leg.setup_s,
         }
         print(json.dumps(result), flush=True)
-    batch.close()
+    if weak is None:
+        leg.batch.close()
     if world > 1:
         dist.destroy_process_group()
 

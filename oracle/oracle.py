@@ -2,9 +2,9 @@
 
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 ``--impl reference`` legs use this module, as the checker / CPU baseline.  It
-consumes the same ``PackedWorlds`` tables as the GPU (original road order, no
-grid) and keeps its own FP64 state.  Observations are float64 (the
-reference's dtype).
+builds its OWN World.__init__ tables from the raw scene (oracle/tables.py:
+numpy + the standard library, no product code, no CUDA library) and keeps
+its own FP64 state.  Observations are float64 (the reference's dtype).
 """
 
 from __future__ import annotations
@@ -14,6 +14,8 @@ import os
 import subprocess
 
 import numpy as np
+
+from .tables import build_tables
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "drivesim_oracle.c")
@@ -82,16 +84,30 @@ def _ptr(a):
     return a.ctypes.data_as(_p) if a is not None else None
 
 
-class OracleBatch:
-    """CPU restatement of SimBatch over PackedWorlds (float64 everything)."""
+# the C-ABI enums (include/drivesim_b200.h), restated
+DYN = {"classic": 0, "invertible": 1, "delta_local": 2}
+COLL = {"ignore": 0, "remove_agent": 1, "end_episode": 2}
+OBS = {"radial": 0, "lidar": 1, "view_cone": 2}
 
-    def __init__(self, packed, cfg, n_threads: int = 0):
-        from paper_2408_01584_b200.config import obs_width
-        from paper_2408_01584_b200 import _native as N
-        self.pw = packed
+
+def obs_width(o) -> int:
+    """observation.py:84-99: ego 7 + partner slots x 7 + road slots x 11, or ego + rays x 5."""
+    if o.mode == "radial":
+        return 7 + 7 * o.max_agents_obs + 11 * o.max_road_points_obs
+    return 7 + 5 * o.n_rays
+
+
+class OracleBatch:
+    """CPU restatement of SimBatch (float64 everything) over a raw scene batch
+    (anything with the RawWorlds attributes)."""
+
+    def __init__(self, raw, cfg, n_threads: int = 0):
+        if not hasattr(raw, "log_x"):
+            raise TypeError("OracleBatch takes the raw scene batch (it builds its own tables)")
+        self.pw = build_tables(raw, cfg)
         self.cfg = cfg
         self.n_threads = n_threads
-        pw = packed
+        pw = self.pw
         self._arrays = {}
         tab = OrTables()
         tab.n_worlds, tab.n_agents, tab.n_rows = pw.n_worlds, pw.n_agents, pw.n_controlled
@@ -104,9 +120,9 @@ class OracleBatch:
         self.tab = tab
         c = OrConfig()
         o = cfg.obs
-        c.dynamics = N.DYN[cfg.dynamics]
-        c.collision_behavior = N.COLL[cfg.collision_behavior]
-        c.obs_mode = N.OBS[o.mode]
+        c.dynamics = DYN[cfg.dynamics]
+        c.collision_behavior = COLL[cfg.collision_behavior]
+        c.obs_mode = OBS[o.mode]
         c.n_rays, c.max_agents_obs, c.max_road_points_obs = o.n_rays, o.max_agents_obs, \
             o.max_road_points_obs
         c.obs_width = obs_width(o)

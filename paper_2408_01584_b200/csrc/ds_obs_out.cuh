@@ -25,10 +25,12 @@ __device__ __forceinline__ int out_row_phase(const ObsOut &o, int64_t orow) {
   return (int)((reinterpret_cast<uintptr_t>(out) >> 2) & 3);
 }
 
-// normalisation by the env's per-column divisors (env.py:50-63): the fast
-// reciprocal-multiply division (<= 2 ulp; the divisors are O(1..100))
+// normalisation by the env's per-column divisors (env.py:50-63): IEEE
+// round-to-nearest division, so a float32 result stays within 1.5 ulp of the
+// reference's float64 quotient (the staged value's own rounding plus one),
+// and a bfloat16 row is exactly the float32 row rounded to bf16
 __device__ __forceinline__ float scaled(const float *row, const float *scale, int c) {
-  return scale ? __fdividef(row[c], scale[c]) : row[c];
+  return scale ? __fdiv_rn(row[c], scale[c]) : row[c];
 }
 
 // Warp-collective: row[0, width) (divided by scale[c] when scale != NULL) to
@@ -54,10 +56,10 @@ __device__ __forceinline__ void write_row(const ObsOut &o, int64_t orow, const f
       for (int q = 0; q < nv; ++q) {
         float4 x = rv[32 * q];
         const float *sc = scale + head + 4 * (lane + 32 * q);
-        x.x = __fdividef(x.x, sc[0]);
-        x.y = __fdividef(x.y, sc[1]);
-        x.z = __fdividef(x.z, sc[2]);
-        x.w = __fdividef(x.w, sc[3]);
+        x.x = __fdiv_rn(x.x, sc[0]);
+        x.y = __fdiv_rn(x.y, sc[1]);
+        x.z = __fdiv_rn(x.z, sc[2]);
+        x.w = __fdiv_rn(x.w, sc[3]);
         ov[32 * q] = x;
       }
     }
@@ -76,14 +78,14 @@ __device__ __forceinline__ void write_row(const ObsOut &o, int64_t orow, const f
     float4 b = reinterpret_cast<const float4 *>(row)[2 * v + 1];
     if (scale) {
       const float *sc = scale + 8 * v;
-      a.x = __fdividef(a.x, sc[0]);
-      a.y = __fdividef(a.y, sc[1]);
-      a.z = __fdividef(a.z, sc[2]);
-      a.w = __fdividef(a.w, sc[3]);
-      b.x = __fdividef(b.x, sc[4]);
-      b.y = __fdividef(b.y, sc[5]);
-      b.z = __fdividef(b.z, sc[6]);
-      b.w = __fdividef(b.w, sc[7]);
+      a.x = __fdiv_rn(a.x, sc[0]);
+      a.y = __fdiv_rn(a.y, sc[1]);
+      a.z = __fdiv_rn(a.z, sc[2]);
+      a.w = __fdiv_rn(a.w, sc[3]);
+      b.x = __fdiv_rn(b.x, sc[4]);
+      b.y = __fdiv_rn(b.y, sc[5]);
+      b.z = __fdiv_rn(b.z, sc[6]);
+      b.w = __fdiv_rn(b.w, sc[7]);
     }
     __nv_bfloat162 q[4] = {__floats2bfloat162_rn(a.x, a.y), __floats2bfloat162_rn(a.z, a.w),
                            __floats2bfloat162_rn(b.x, b.y), __floats2bfloat162_rn(b.z, b.w)};

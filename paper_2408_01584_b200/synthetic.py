@@ -14,7 +14,10 @@ the survey's recipe:
   U(-pi, pi], speed U[2, 15] m/s;
 * T-step logs from a classic-bicycle rollout with a = 0 and a constant steer
   U(-0.1, 0.1), all valid; goal = final logged position;
-* every coordinate quantised to 2^-10 m (lossless in float32).
+* every coordinate quantised to 2^-10 m (lossless in float32) -- or, with
+  ``quantize=False``, left at full FP64 resolution (off-lattice: the float32
+  copies the kernels cull with carry a non-zero rounding error, as real
+  prepared / WOMD inputs do).
 
 A world's content depends only on (seed, global world id), so a world shard
 generated on any rank is identical to the same world generated anywhere else.
@@ -27,7 +30,6 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _native
 from .config import OBJECT_KINDS, ROAD_KINDS
 from .packing import RawWorlds, _offsets
 
@@ -45,6 +47,7 @@ class WaymoSpec:
     dt: float = 0.1
     world_offset: int = 0       # global id of the first world (sharding)
     map_side: float | None = None
+    quantize: bool = True       # False: off-lattice FP64 coordinates
 
     @property
     def side(self) -> float:
@@ -53,8 +56,8 @@ class WaymoSpec:
         return 40.0 * math.sqrt(self.n_points / 100.0) + 60.0
 
 
-def _quant(v):
-    return np.round(np.asarray(v) / Q) * Q
+def _quant(v, on: bool = True):
+    return np.round(np.asarray(v) / Q) * Q if on else np.asarray(v, np.float64)
 
 
 def _world_params(spec: WaymoSpec, wid: int):
@@ -66,8 +69,9 @@ def _world_params(spec: WaymoSpec, wid: int):
     kind = np.where(u < 0.8, 0, np.where(u < 0.9, 1, 2)).astype(np.int8)
     length = np.where(kind == 0, 4.6 + rng.uniform(-0.3, 0.3, A), np.where(kind == 1, 0.8, 1.8))
     width = np.where(kind == 0, 1.8, np.where(kind == 1, 0.8, 0.6))
-    x = _quant(rng.uniform(0.25 * L, 0.75 * L, A))
-    y = _quant(rng.uniform(0.25 * L, 0.75 * L, A))
+    q = spec.quantize
+    x = _quant(rng.uniform(0.25 * L, 0.75 * L, A), q)
+    y = _quant(rng.uniform(0.25 * L, 0.75 * L, A), q)
     h = -rng.uniform(-math.pi, math.pi, A)          # (-pi, pi]
     v = rng.uniform(2.0, 15.0, A)
     steer = rng.uniform(-0.1, 0.1, A)
@@ -105,7 +109,7 @@ def _world_params(spec: WaymoSpec, wid: int):
     px = px - np.repeat(px[first], lens) + start[poly_of, 0]
     py = py - np.repeat(py[first], lens) + start[poly_of, 1]
     return dict(kind=kind, length=length, width=width, x=x, y=y, h=h, v=v, steer=steer,
-                lens=lens, pkind=kinds, px=_quant(px), py=_quant(py))
+                lens=lens, pkind=kinds, px=_quant(px, q), py=_quant(py, q))
 
 
 def generate(spec: WaymoSpec) -> RawWorlds:
@@ -126,7 +130,7 @@ def generate(spec: WaymoSpec) -> RawWorlds:
         cy = cy + v * np.sin(ch + beta) * spec.dt
         ch = np.mod(ch + turn + math.pi, 2 * math.pi) - math.pi
         ch = np.where(ch <= -math.pi, ch + 2 * math.pi, ch)
-    lx, ly = _quant(lx), _quant(ly)
+    lx, ly = _quant(lx, spec.quantize), _quant(ly, spec.quantize)
     vx = v[:, None] * np.cos(lh)
     vy = v[:, None] * np.sin(lh)
     goal = np.stack([lx[:, -1], ly[:, -1]], -1)
@@ -141,9 +145,11 @@ def generate(spec: WaymoSpec) -> RawWorlds:
         log_valid=np.ones(N * T, bool), poly_off=_offsets([len(l) for l in lens]),
         poly_kind=cat("pkind"), poly_pt_off=_offsets(np.concatenate(lens)), pt_x=cat("px"),
         pt_y=cat("py"))
-    # mark_controllable (scenario.py:371-384) with the default 2.0 m threshold
-    d = _native.host_hypot_cpython(lx[:, 0] - goal[:, 0], ly[:, 0] - goal[:, 1])
-    raw.controllable = d > 2.0
+    # mark_controllable (scenario.py:371-384) with the default 2.0 m threshold;
+    # the reference's distance is CPython's math.hypot (pure Python here, so
+    # generating a scene never loads the CUDA library)
+    d = np.frompyfunc(math.hypot, 2, 1)(lx[:, 0] - goal[:, 0], ly[:, 0] - goal[:, 1])
+    raw.controllable = d.astype(np.float64) > 2.0
     return raw
 
 

@@ -8,9 +8,9 @@ import math
 import numpy as np
 
 F32_ULPS = 2
-OBS_ABS = 1e-5     # absolute floor of the FP32 observation tolerance
+OBS_ABS = 1e-6     # absolute floor of the FP32 observation tolerance
 POS_TOL = 1e-9     # metres, free-run pose tolerance after a full episode
-ANG_TOL = 1e-11    # radians
+ANG_TOL = 1e-12    # radians
 
 
 def obs_tolerance(ref64: np.ndarray) -> np.ndarray:

@@ -36,14 +36,14 @@ def _single_point_roads(raw: RawWorlds, rng) -> RawWorlds:
     return raw
 
 
-def ragged_batch(seed: int = 0, num_steps: int = 91) -> RawWorlds:
+def ragged_batch(seed: int = 0, num_steps: int = 91, quantize: bool = True) -> RawWorlds:
     rng = np.random.default_rng(seed)
     specs = [(1, 0), (5, 3), (33, 400), (130, 5000), (17, 1), (300, 2500), (64, 64), (2, 900)]
     parts = []
     for k, (A, P) in enumerate(specs):
         if P == 0:
             raw = generate(WaymoSpec(n_worlds=1, n_agents=A, n_points=12, seed=seed,
-                                     world_offset=k, num_steps=num_steps))
+                                     world_offset=k, num_steps=num_steps, quantize=quantize))
             raw.poly_off = np.zeros(2, np.int64)
             raw.poly_kind = raw.poly_kind[:0]
             raw.poly_pt_off = np.zeros(1, np.int64)
@@ -51,7 +51,7 @@ def ragged_batch(seed: int = 0, num_steps: int = 91) -> RawWorlds:
             raw.pt_y = raw.pt_y[:0]
         elif P < 10:
             raw = generate(WaymoSpec(n_worlds=1, n_agents=A, n_points=12, seed=seed,
-                                     world_offset=k, num_steps=num_steps))
+                                     world_offset=k, num_steps=num_steps, quantize=quantize))
             raw.poly_off = np.array([0, 1], np.int64)
             raw.poly_kind = raw.poly_kind[:1]
             raw.poly_pt_off = np.array([0, P], np.int64)
@@ -59,7 +59,7 @@ def ragged_batch(seed: int = 0, num_steps: int = 91) -> RawWorlds:
             raw.pt_y = raw.pt_y[:P].copy()
         else:
             raw = generate(WaymoSpec(n_worlds=1, n_agents=A, n_points=P, seed=seed,
-                                     world_offset=k, num_steps=num_steps))
+                                     world_offset=k, num_steps=num_steps, quantize=quantize))
         T = num_steps
         valid = raw.log_valid.reshape(A, T)
         for i in range(A):

@@ -97,8 +97,8 @@ class Runner:
             self.pw = self.b.packed
         else:
             from oracle.oracle import OracleBatch
-            self.pw = pack(raw, cfg)
-            self.b = OracleBatch(self.pw, cfg)
+            self.b = OracleBatch(raw, cfg)
+            self.pw = self.b.pw
         self.n_controlled = self.pw.n_controlled
 
     def _state(self, name):

@@ -3,6 +3,7 @@ the kernels query (every point in its cell, every segment in every cell its
 AABB touches), and the float2 rounding bound is what the key analysis uses."""
 
 import numpy as np
+import pytest
 
 from paper_2408_01584_b200.config import ROAD_EDGE, SimConfig
 from paper_2408_01584_b200.device_layout import build_layout
@@ -10,8 +11,8 @@ from paper_2408_01584_b200.packing import pack
 from paper_2408_01584_b200.synthetic import WaymoSpec, generate
 
 
-def _pw():
-    raw = generate(WaymoSpec(n_worlds=3, n_agents=16, n_points=900, seed=4))
+def _pw(quantize=True):
+    raw = generate(WaymoSpec(n_worlds=3, n_agents=16, n_points=900, seed=4, quantize=quantize))
     return pack(raw, SimConfig(init_mode="all_valid"))
 
 
@@ -59,13 +60,16 @@ def test_edge_segments_binned_into_every_touched_cell():
                             np.isclose(lay.eseg_by[sl], pw.seg_by[k])).any()
 
 
-def test_float2_rounding_bound():
-    pw = _pw()
+@pytest.mark.parametrize("quantize", [True, False])
+def test_float2_rounding_bound(quantize):
+    pw = _pw(quantize)
     lay = build_layout(pw, 8.0)
     for w in range(pw.n_worlds):
         p0, p1 = pw.p_off[w], pw.p_off[w + 1]
         ex = np.abs(lay.gpt_xy[p0:p1, 0].astype(np.float64) - (lay.gpt_x[p0:p1] - lay.grid_x0[w]))
         ey = np.abs(lay.gpt_xy[p0:p1, 1].astype(np.float64) - (lay.gpt_y[p0:p1] - lay.grid_y0[w]))
         assert max(ex.max(), ey.max()) == lay.grid_eps[w]
-    # quantised synthetic coordinates are exact in float32
-    assert (lay.grid_eps == 0).all()
+    if quantize:   # quantised synthetic coordinates are exact in float32
+        assert (lay.grid_eps == 0).all()
+    else:          # off-lattice: the key bound's eps_p term is live
+        assert (lay.grid_eps > 0).all() and (lay.grid_eps < 1e-4).all()

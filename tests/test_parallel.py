@@ -51,7 +51,7 @@ def _worker(rank, world, port, q):
     # each rank generates ONLY its own world ids (global seeds) and steps them
     raw = generate(WaymoSpec(n_worlds=hi - lo, n_agents=16, n_points=300, seed=3,
                              world_offset=lo, num_steps=12))
-    ora = OracleBatch(pack(raw, cfg), cfg)
+    ora = OracleBatch(raw, cfg)
     rng = np.random.default_rng(100 + lo)
     for _ in range(12):
         ora.step(rng.uniform(-1, 1, (ora.pw.n_controlled, 2)))
@@ -93,7 +93,7 @@ def test_two_rank_gloo_shards_and_stats():
     for lo, hi in ((lo0, hi0), (lo1, hi1)):
         raw = generate(WaymoSpec(n_worlds=hi - lo, n_agents=16, n_points=300, seed=3,
                                  world_offset=lo, num_steps=12))
-        ora = OracleBatch(pack(raw, cfg), cfg)
+        ora = OracleBatch(raw, cfg)
         rng = np.random.default_rng(100 + lo)
         for _ in range(12):
             ora.step(rng.uniform(-1, 1, (ora.pw.n_controlled, 2)))
