@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define DS_ABI_VERSION 3
+#define DS_ABI_VERSION 4
 #define DS_MAX_AGENTS_PER_WORLD 1024
 
 /* error codes */
@@ -169,7 +169,16 @@ typedef struct ds_state {
    * at; results never depend on it (it only narrows a provably sufficient
    * search disc).  NULL disables it. */
   float *obs_hint;
+  /* one device word of sticky DS_STATUS_* bits set by the kernels (read and
+   * cleared with ds_status); NULL disables the reporting */
+  uint32_t *status;
 } ds_state;
+
+/* ds_state.status bits */
+#define DS_STATUS_BAD_ACTION_INDEX 1u  /* a joint action index outside the grid:
+                                        * the reference's to_continuous raises
+                                        * IndexError (env.py:111-116); the
+                                        * agent's dynamics are skipped */
 
 /* Per-call step arguments. */
 typedef struct ds_step_args {
@@ -249,6 +258,24 @@ int ds_set_obs_format(ds_handle *h, int dtype, int row_stride);
  * (ippo.py:136-142); this is the in-loop sampler of the device rollout. */
 int ds_sample_categorical(const void *logits, int dtype, int64_t rows, int32_t n, int64_t ld,
                           uint64_t seed, uint64_t counter, int32_t *out, void *stream);
+
+/* Copy the handle's sticky status word (DS_STATUS_* bits) to host *out,
+ * optionally clearing it; synchronises `stream`.  *out = 0 when the state
+ * has no status word. */
+int ds_status(ds_handle *h, uint32_t *out, int clear, void *stream);
+
+/* Gumbel noise of raw 32-bit hash values, out[i] = -log(-log u(bits[i])) with
+ * u = (2 (bits >> 9) + 1) 2^-24 strictly inside (0, 1): the noise function
+ * of ds_sample_categorical, exposed so tests can feed it the extreme hash
+ * values.  bits, out: device arrays of n elements. */
+int ds_gumbel_noise(const uint32_t *bits, int64_t n, float *out, void *stream);
+
+/* goal_seek policy (make_policy("goal_seek"), engine.py:554-574): actions
+ * [n_rows, 2] float32 (accel, steer) for every controlled row from the
+ * handle's current device state -- proportional steer-to-goal, speed capped
+ * by the distance to the goal -- written to device `actions` on `stream`,
+ * ready for ds_step.  Stream-ordered, no host sync. */
+int ds_goal_seek(ds_handle *h, float *actions, void *stream);
 
 /* Batched polyline decimation (preprocess, scenario.py:387-411, with
  * decimate_polyline, geometry.py:84-127): for every polyline p (points

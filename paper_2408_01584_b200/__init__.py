@@ -10,14 +10,15 @@ from .config import (EGO_WIDTH, PARTNER_WIDTH, RAY_WIDTH, ROAD_SLOT_WIDTH, ObsCo
 
 __all__ = ["SimConfig", "ObsConfig", "ObsLayout", "layout", "obs_width", "EGO_WIDTH",
            "PARTNER_WIDTH", "ROAD_SLOT_WIDTH", "RAY_WIDTH", "SimBatch", "init_batch",
-           "benchmark", "VecDriveEnv", "EnvConfig", "HostStepper"]
+           "benchmark", "make_policy", "goal_seek_actions", "VecDriveEnv", "EnvConfig",
+           "HostStepper"]
 
 
 def __getattr__(name):
     # engine/env import torch; keep `import paper_2408_01584_b200` light.
     if name in ("SimBatch", "init_batch", "benchmark", "StepOutput", "EpisodeInfo", "Metrics",
                 "ThroughputReport", "compute_metrics", "ActionCountMismatch", "HostStepper",
-                "HostStepResult"):
+                "HostStepResult", "make_policy", "goal_seek_actions"):
         from . import engine
         return getattr(engine, name)
     if name in ("VecDriveEnv", "EnvConfig", "ActionGrid"):

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # DS_LIB_PATH (dev only): an alternative build of the same library, for A/B timing
 LIB_PATH = os.environ.get("DS_LIB_PATH") or os.path.join(_HERE, "libdrivesim_b200.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
 OBS_F32, OBS_BF16 = 0, 1   # ds_set_obs_format element types
 
 DS_OK = 0
@@ -81,7 +81,11 @@ STATE_PTRS = ["x", "y", "heading", "speed", "head_angle", "flags", "t", "episode
 
 class DsState(C.Structure):
     _fields_ = [(n, _p) for n in STATE_PTRS] + [("ring_cap", C.c_int32),
-                                                ("reserved0", C.c_int32), ("obs_hint", _p)]
+                                                ("reserved0", C.c_int32), ("obs_hint", _p),
+                                                ("status", _p)]
+
+
+STATUS_BAD_ACTION_INDEX = 1
 
 
 class DsStepArgs(C.Structure):
@@ -94,7 +98,7 @@ class DsStepArgs(C.Structure):
 
 
 EXPORTS = ["ds_abi_version", "ds_lidar_supported", "ds_struct_sizes", "ds_last_error", "ds_create", "ds_destroy", "ds_reset", "ds_step",
-           "ds_observe", "ds_set_obs_format", "ds_sample_categorical", "ds_decimate_scratch_bytes", "ds_decimate_polylines", "ds_episode_drain", "ds_host_hypot_libm", "ds_host_hypot_cpython",
+           "ds_observe", "ds_set_obs_format", "ds_sample_categorical", "ds_decimate_scratch_bytes", "ds_decimate_polylines", "ds_episode_drain", "ds_status", "ds_gumbel_noise", "ds_goal_seek", "ds_host_hypot_libm", "ds_host_hypot_cpython",
            "ds_host_hypot_port", "ds_host_wrap_port", "ds_host_road_headings"]
 
 _lib = None
@@ -122,6 +126,9 @@ def lib():
     L.ds_episode_drain.argtypes = [_p, _p, C.c_int32, C.POINTER(C.c_int32), _p]
     L.ds_set_obs_format.argtypes = [_p, C.c_int, C.c_int]
     L.ds_decimate_scratch_bytes.argtypes = [C.c_int64]
+    L.ds_gumbel_noise.argtypes = [_p, C.c_int64, _p, _p]
+    L.ds_goal_seek.argtypes = [_p, _p, _p]
+    L.ds_status.argtypes = [_p, _p, C.c_int, _p]
     L.ds_decimate_polylines.argtypes = [_p, _p, _p, C.c_int64, _p, C.c_double, _p, _p,
                                         C.c_int64, _p]
     L.ds_sample_categorical.argtypes = [_p, C.c_int, C.c_int64, C.c_int32, C.c_int64,

@@ -132,6 +132,34 @@ int ds_sample_categorical(const void *logits, int dtype, int64_t rows, int32_t n
   return DS_OK;
 }
 
+int ds_status(ds_handle *h, uint32_t *out, int clear, void *stream) {
+  if (!h || !out) return fail(DS_E_INVALID, "ds_status: null argument");
+  *out = 0;
+  if (!h->st.status) return DS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(out, h->st.status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess && clear) e = cudaMemsetAsync(h->st.status, 0, sizeof(uint32_t), s);
+  if (e != cudaSuccess) return cuda_fail(e, "status");
+  return DS_OK;
+}
+
+int ds_gumbel_noise(const uint32_t *bits, int64_t n, float *out, void *stream) {
+  if (n < 0) return fail(DS_E_INVALID, "ds_gumbel_noise: negative count");
+  if (n > 0 && (!bits || !out)) return fail(DS_E_INVALID, "ds_gumbel_noise: null argument");
+  cudaError_t e = ds::launch_gumbel(bits, n, out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "gumbel kernel");
+  return DS_OK;
+}
+
+int ds_goal_seek(ds_handle *h, float *actions, void *stream) {
+  if (!h) return fail(DS_E_INVALID, "ds_goal_seek: null handle");
+  if (h->tab.n_rows > 0 && !actions) return fail(DS_E_INVALID, "ds_goal_seek: null actions");
+  cudaError_t e = ds::launch_goal_seek(h, actions, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "goal_seek kernel");
+  return DS_OK;
+}
+
 int64_t ds_decimate_scratch_bytes(int64_t n_points) {
   return n_points < 0 ? 0 : n_points * (int64_t)(2 * sizeof(int32_t) + sizeof(double));
 }

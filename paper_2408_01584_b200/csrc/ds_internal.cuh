@@ -45,6 +45,8 @@ cudaError_t launch_decimate(const double *x, const double *y, const int64_t *pol
 cudaError_t launch_sample(const void *logits, int dtype, int64_t rows, int n, int64_t ld,
                           uint64_t seed, uint64_t counter, int32_t *out, cudaStream_t s);
 size_t step_smem_bytes(int max_agents);
+cudaError_t launch_goal_seek(const ds_handle *h, float *out, cudaStream_t s);
+cudaError_t launch_gumbel(const uint32_t *bits, int64_t n, float *out, cudaStream_t s);
 cudaError_t configure_kernels(int max_dynamic_smem);
 cudaError_t configure_step_kernels(int max_dynamic_smem);
 

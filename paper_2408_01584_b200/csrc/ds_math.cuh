@@ -45,6 +45,21 @@ DS_HD double wrap(double theta) {
   return r;
 }
 
+// np.mod(a, 2 pi) (numpy's npy_divmod: fmod, then +2pi for a negative
+// remainder; fmod is exact), the first half of wrap() above.
+DS_HD double floor_mod_2pi(double a) {
+  if (a >= 0.0 && a < kTwoPi) return a;
+  if (a >= kTwoPi && a < 2.0 * kTwoPi) return a - kTwoPi;
+  if (a < 0.0 && a >= -kTwoPi) return a + kTwoPi;
+  double r = fmod(a, kTwoPi);
+  if (r != 0.0) {
+    if (r < 0.0) r += kTwoPi;
+  } else {
+    r = 0.0;
+  }
+  return r;
+}
+
 // hypot with the exact arithmetic of glibc 2.39's non-FMA kernel
 // (sysdeps/ieee754/dbl-64/e_hypot.c), which is what numba's math.hypot,
 // numpy's np.hypot and the oracle's libm call resolve to on this image

@@ -24,7 +24,6 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-// uniform in (0, 1): 24 random bits, centred in their cell
 // 32-bit integer hash (lowbias32): one per logit; the 64-bit key and the row
 // are folded into a per-row seed once
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
@@ -41,10 +40,21 @@ __device__ __forceinline__ uint32_t row_seed(uint64_t key, uint64_t r) {
                                        (uint32_t)(r >> 32)));
 }
 
-// uniform in (0, 1): the top 24 bits, centred
-__device__ __forceinline__ float hash_uniform(uint32_t seed, uint32_t j) {
-  const uint32_t h = hash32(seed + j * 0x9e3779b9u);
-  return ((float)(h >> 8) + 0.5f) * 5.9604644775390625e-8f;
+__device__ __forceinline__ uint32_t hash_bits(uint32_t seed, uint32_t j) {
+  return hash32(seed + j * 0x9e3779b9u);
+}
+
+// Gumbel noise -log(-log u) of one 32-bit hash.  u = (2m + 1) 2^-24 from the
+// top 23 bits m: exactly representable and strictly inside (0, 1)
+// (2^-24 <= u <= 1 - 2^-24).  The exponential variate -log u is formed as
+// -log1p(-w) from w = 1 - u = (2^24 - 2m - 1) 2^-24, also exact, so it stays
+// accurate (and > 0) right up to u = 1 - 2^-24 where -log u ~ 6e-8; the
+// outer log is the accurate logf, never the fast __logf.
+__device__ __forceinline__ float gumbel_of_bits(uint32_t h) {
+  const uint32_t m = h >> 9;
+  const float w = (float)(16777215u - 2u * m) * 5.9604644775390625e-8f;
+  const float e = -log1pf(-w);
+  return -logf(e);
 }
 
 template <typename T>
@@ -68,9 +78,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32) sample_kernel(const T *logi
   int arg = 0x7fffffff;
   const uint32_t seed = row_seed(key, (uint64_t)r);
   for (int j = lane; j < n; j += 32) {
-    const float u = hash_uniform(seed, (uint32_t)j);
-    // Gumbel noise -log(-log u) with the hardware log2 (u in (0, 1): -log u > 0)
-    const float v = load_logit(row + j) - __logf(-__logf(u));
+    const float v = load_logit(row + j) + gumbel_of_bits(hash_bits(seed, (uint32_t)j));
     if (v > best || (v == best && j < arg) || arg == 0x7fffffff) {
       best = v;
       arg = j;
@@ -88,7 +96,18 @@ __global__ void __launch_bounds__(kSampleWarps * 32) sample_kernel(const T *logi
   if (lane == 0) out[r] = arg;
 }
 
+__global__ void gumbel_kernel(const uint32_t *bits, int64_t n, float *out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = gumbel_of_bits(bits[i]);
+}
+
 }  // namespace
+
+cudaError_t launch_gumbel(const uint32_t *bits, int64_t n, float *out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  gumbel_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(bits, n, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_sample(const void *logits, int dtype, int64_t rows, int n, int64_t ld,
                           uint64_t seed, uint64_t counter, int32_t *out, cudaStream_t s) {

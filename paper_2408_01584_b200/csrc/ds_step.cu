@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(MAXT, MINB) step_kernel(ds_tables T, ds_config
     if (!a.replay && live) {
       // Action row (engine.py:392: float64 cast of the caller's values).
       double a0v = 0.0, a1v = 0.0, a2v = 0.0, a3v = 0.0;
+      bool bad_action = false;
       if (a.actions) {
         const float *ar = a.actions + (int64_t)row * a.act_dim;
         a0v = ar[0];
@@ -247,17 +248,27 @@ __global__ void __launch_bounds__(MAXT, MINB) step_kernel(ds_tables T, ds_config
         if (a.act_dim > 2) a2v = ar[2];
         if (a.act_dim > 3) a3v = ar[3];
       } else {
-        // VecDriveEnv.to_continuous (env.py:111-116): divmod by n_steer.
-        int idx = a.action_idx[row];
+        // VecDriveEnv.to_continuous (env.py:111-116): accel[i // n_steer],
+        // steer[i % n_steer] with Python floor division and numpy indexing
+        // (a negative accel index counts from the end; outside
+        // [-n_accel, n_accel) numpy raises IndexError: flagged in the
+        // status word, the agent's dynamics skipped, never clamped)
+        const int idx = a.action_idx[row];
         int ai = idx >= 0 ? idx / a.n_steer : -((-idx + a.n_steer - 1) / a.n_steer);
-        int si = idx - ai * a.n_steer;
-        if (ai < 0) ai += a.n_accel;
-        ai = min(max(ai, 0), a.n_accel - 1);
-        a0v = a.grid_accel[ai];
-        a1v = a.grid_steer[si];
+        const int si = idx - ai * a.n_steer;
+        if (ai < -a.n_accel || ai >= a.n_accel) {
+          if (S.status) atomicOr(S.status, DS_STATUS_BAD_ACTION_INDEX);
+          bad_action = true;
+        } else {
+          if (ai < 0) ai += a.n_accel;
+          a0v = a.grid_accel[ai];
+          a1v = a.grid_steer[si];
+        }
       }
       const double L = T.length[g];
-      if (C.dynamics == DS_DYN_CLASSIC) {
+      if (bad_action) {
+        // pose held (the reference would have raised before stepping)
+      } else if (C.dynamics == DS_DYN_CLASSIC) {
         // classic_core (fp:319-333), left-to-right, no FMA.
         const double acc = clip(a0v, C.accel_lo, C.accel_hi);
         const double delta = clip(a1v, C.steer_lo, C.steer_hi);
@@ -484,6 +495,36 @@ __global__ void __launch_bounds__(1024) reset_kernel(ds_tables T, ds_state S, co
     S.t[w] = 0;
     S.episode_over[w] = 0;
   }
+}
+
+// goal_seek_actions (engine.py:559-574): proportional steer-to-goal with the
+// speed capped by the distance, one thread per controlled row, FP64 in the
+// reference's operation order (distance: the glibc hypot port; err =
+// floor-mod(atan2(dy, dx) - heading + pi, 2 pi) - pi, WITHOUT wrap()'s
+// r <= -pi correction, as np.mod there).  Rows of done / removed agents get
+// the same formula (the reference computes all controlled rows; the step
+// ignores them).  Output: float32 [rows, 2] (accel, steer), the action format
+// ds_step consumes.
+__global__ void goal_seek_kernel(ds_tables T, ds_config C, ds_state S, float *out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= T.n_rows) return;
+  const int64_t g = T.row_agent[r];
+  const double dx = T.goal_x[g] - S.x[g];
+  const double dy = T.goal_y[g] - S.y[g];
+  const double dist = hypot(dx, dy);
+  const double err = floor_mod_2pi(atan2(dy, dx) - S.heading[g] + kPi) - kPi;
+  const double steer = fmin(fmax(2.0 * err, C.steer_lo), C.steer_hi);
+  const double target_v = fmin(0.8 * dist + 0.5, 15.0);
+  const double accel = fmin(fmax(2.0 * (target_v - S.speed[g]), C.accel_lo), C.accel_hi);
+  out[2 * (int64_t)r] = (float)accel;
+  out[2 * (int64_t)r + 1] = (float)steer;
+}
+
+cudaError_t launch_goal_seek(const ds_handle *h, float *out, cudaStream_t s) {
+  const int n = h->tab.n_rows;
+  if (n <= 0) return cudaSuccess;
+  goal_seek_kernel<<<(n + 127) / 128, 128, 0, s>>>(h->tab, h->cfg, h->st, out);
+  return cudaGetLastError();
 }
 
 cudaError_t configure_step_kernels(int max_dynamic_smem) {

@@ -253,6 +253,11 @@ class SimBatch:
                                                   all_segments=cfg.obs.mode != "radial")
         self._upload()
         self._episode_infos: list = []
+        # the batch keeps every finished episode (SimBatch.episode_infos,
+        # engine.py:614, 647); VecDriveEnv turns this off and hands each
+        # step's records out instead (the reference env clears the list every
+        # step, env.py:103-104), so a long rollout does not grow host memory
+        self.log_episodes = True
         self._by_serial: dict = {}
         self._serial = 0
         self._steps_since_drain = 0
@@ -335,6 +340,8 @@ class SimBatch:
         st.ring_cap = self._ring_cap
         self._hint = torch.zeros((max(n, 1), 4), dtype=torch.float32, device=dev)
         st.obs_hint = self._hint.data_ptr()
+        self._status = torch.zeros(1, dtype=torch.int32, device=dev)
+        st.status = self._status.data_ptr()
         self._state = st
 
         # Outputs (reused every call, like the reference's buffers).
@@ -348,6 +355,30 @@ class SimBatch:
         self._mask = torch.zeros(W, dtype=torch.uint8, device=dev)
 
     # -- stepping ----------------------------------------------------------
+
+    def _arg(self, t, dtype, numel: int, name: str, convert: bool = False):
+        """A kernel argument tensor checked before its raw pointer is taken:
+        on this batch's device, of ``dtype`` (converted when ``convert`` and
+        the conversion is exact), contiguous, at least ``numel`` elements.
+        Returns the (possibly converted) tensor; the caller keeps it alive."""
+        if not torch.is_tensor(t):
+            raise TypeError(f"{name}: expected a torch tensor")
+        if t.device != self.device:
+            raise ValueError(f"{name}: on {t.device}, the batch is on {self.device}")
+        if t.dtype != dtype:
+            if not convert:
+                raise ValueError(f"{name}: dtype {t.dtype}, expected {dtype}")
+            t = t.to(dtype)
+        if not t.is_contiguous():
+            if not convert:
+                raise ValueError(f"{name}: must be contiguous")
+            t = t.contiguous()
+        if t.numel() < numel:
+            raise ValueError(f"{name}: {t.numel()} elements, needs {numel}")
+        return t
+
+    def _sel_w(self) -> int:
+        return self.cfg.obs.max_agents_obs + self.cfg.obs.max_road_points_obs
 
     def _stream(self):
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
@@ -370,6 +401,9 @@ class SimBatch:
                 raise ActionCountMismatch(
                     f"expected {self.n_controlled} action rows, got {idx.shape[0]}")
             accel, steer = grid
+            accel = self._arg(accel, torch.float64, 1, "grid accel", convert=True)
+            steer = self._arg(steer, torch.float64, 1, "grid steer", convert=True)
+            keep += [accel, steer]
             a.action_idx = idx.data_ptr()
             a.grid_accel = accel.data_ptr()
             a.grid_steer = steer.data_ptr()
@@ -388,6 +422,11 @@ class SimBatch:
             a.actions = act.data_ptr()
             a.act_dim = act.shape[1]
             keep.append(act)
+        if obs_scale is not None:
+            obs_scale = self._arg(obs_scale, torch.float32, self.width, "obs_scale", convert=True)
+            keep.append(obs_scale)
+        if sel_idx is not None:
+            sel_idx = self._arg(sel_idx, torch.int32, self.n_controlled * self._sel_w(), "sel_idx")
         self._maybe_drain()
         a.obs = self.observations.data_ptr()
         a.rewards = self.rewards.data_ptr()
@@ -412,8 +451,14 @@ class SimBatch:
         recompute their observation rows; their rewards/dones rows read 0."""
         self._check_open()
         mask_ptr = None
+        if obs_scale is not None:
+            obs_scale = self._arg(obs_scale, torch.float32, self.width, "obs_scale", convert=True)
+        if sel_idx is not None:
+            sel_idx = self._arg(sel_idx, torch.int32, self.n_controlled * self._sel_w(), "sel_idx")
         if world_mask is not None:
-            mask_ptr = world_mask.to(torch.uint8).contiguous().data_ptr()
+            world_mask = self._arg(world_mask, torch.uint8, self.n_worlds, "world_mask",
+                                   convert=True)
+            mask_ptr = world_mask.data_ptr()
         elif world_ids is not None:
             ids = torch.as_tensor(list(world_ids) if not torch.is_tensor(world_ids) else world_ids,
                                   dtype=torch.int64)
@@ -446,6 +491,11 @@ class SimBatch:
         return self.observations
 
     def observe(self, obs_scale=None, sel_idx=None):
+        self._check_open()
+        if obs_scale is not None:
+            obs_scale = self._arg(obs_scale, torch.float32, self.width, "obs_scale", convert=True)
+        if sel_idx is not None:
+            sel_idx = self._arg(sel_idx, torch.int32, self.n_controlled * self._sel_w(), "sel_idx")
         N.check(N.lib().ds_observe(self._handle, None, self.observations.data_ptr(),
                                    obs_scale.data_ptr() if obs_scale is not None else None,
                                    sel_idx.data_ptr() if sel_idx is not None else None,
@@ -466,13 +516,25 @@ class SimBatch:
             names = self.packed.names
             for serial, w, nc, ng, nv, no in recs.tolist():
                 e = EpisodeInfo(names[w], w, nc, ng, nv, no)
-                self._episode_infos.append(e)
+                if self.log_episodes:
+                    self._episode_infos.append(e)
                 self._by_serial.setdefault(serial, []).append(e)
         # keep per-step lists only for the recent window (lazy env readers)
         old = [k for k in self._by_serial if k < self._serial - 4 * self.RING_STEPS]
         for k in old:
             del self._by_serial[k]
         N.check(rc, "ds_episode_drain")
+        self.check_status()
+
+    def check_status(self):
+        """Raise the errors the kernels flagged since the last check (a host
+        synchronisation): IndexError for a joint action index outside the
+        action grid, as the reference's to_continuous (env.py:111-116)."""
+        st = C.c_uint32(0)
+        N.check(N.lib().ds_status(self._handle, C.byref(st), 1, self._stream()), "ds_status")
+        if st.value & N.STATUS_BAD_ACTION_INDEX:
+            raise IndexError("a joint action index was outside the action grid "
+                             "(those agents were not advanced)")
 
     def episodes_of_step(self, serial: int) -> list:
         """Episode records finished during step ``serial`` (synchronises)."""
@@ -541,32 +603,64 @@ def random_actions(n_rows: int, cfg: SimConfig, seed: int, t: int, device) -> to
     return lo + (hi - lo) * u
 
 
+def goal_seek_actions(batch: "SimBatch", out: torch.Tensor | None = None) -> torch.Tensor:
+    """goal_seek_actions (engine.py:559-574) for every controlled row of
+    ``batch`` from its current device state: float32 [n_controlled, 2]
+    (accel, steer) on the device, one ds_goal_seek launch, no host sync."""
+    batch._check_open()
+    n = batch.n_controlled
+    if out is None:
+        out = torch.empty((max(n, 1), 2), dtype=torch.float32, device=batch.device)[:n]
+    if out.shape != (n, 2) or out.dtype != torch.float32 or not out.is_contiguous() \
+            or out.device != batch.device:
+        raise ValueError("goal_seek_actions: out must be a contiguous float32 [n, 2] device tensor")
+    N.check(N.lib().ds_goal_seek(batch._handle, C.c_void_p(out.data_ptr()), batch._stream()),
+            "ds_goal_seek")
+    return out
+
+
+def make_policy(spec: str, cfg: SimConfig, batch: "SimBatch", seed: int = 0):
+    """make_policy (engine.py:535-556) over a whole batch: callable(t) ->
+    device actions [n_controlled, 2] (or None for replay).  Specs "random"
+    (uniform over the bounds, counter-based in (seed, row, t)), "replay",
+    "constant[:a:s]", "goal_seek"."""
+    n, dev = batch.n_controlled, batch.device
+    if spec == "replay":
+        return lambda t: None
+    if spec == "random":
+        return lambda t: random_actions(n, cfg, seed, t, dev)
+    if spec.startswith("constant"):
+        parts = spec.split(":")
+        a = float(parts[1]) if len(parts) > 1 else 0.0
+        s = float(parts[2]) if len(parts) > 2 else 0.0
+        const = torch.tensor([[a, s]], dtype=torch.float32, device=dev).repeat(n, 1)
+        return lambda t: const
+    if spec == "goal_seek":
+        buf = torch.empty((max(n, 1), 2), dtype=torch.float32, device=dev)[:n]
+        return lambda t: goal_seek_actions(batch, buf)
+    raise ValueError(f"unknown policy {spec!r}")
+
+
 def benchmark(scenarios: list, cfg: SimConfig, worlds: int, steps: int, policy: str = "random",
               n_workers=None, seed: int | None = None, device=None) -> ThroughputReport:
     """engine.py:811-857 on the GPU: step ``worlds`` worlds ``steps`` times
-    under a trivial policy with observations every step and auto-reset;
-    elapsed time from CUDA events (init/upload excluded)."""
+    under a trivial policy (make_policy) with observations every step and
+    auto-reset; elapsed time from CUDA events (init/upload excluded)."""
     if worlds < 1 or steps < 1:
         raise ValueError("worlds and steps must be >= 1")
     seed = cfg.seed if seed is None else seed
     chosen = [scenarios[w % len(scenarios)] for w in range(worlds)]
     batch = SimBatch(chosen, cfg, device=device)
     dev = batch.device
-    acts = None
-    if policy == "random":
-        acts = [random_actions(batch.n_controlled, cfg, seed, t, dev) for t in range(min(steps, 8))]
-    elif policy.startswith("constant"):
-        parts = policy.split(":")
-        a = float(parts[1]) if len(parts) > 1 else 0.0
-        s = float(parts[2]) if len(parts) > 2 else 0.0
-        acts = [torch.tensor([[a, s]], device=dev).repeat(batch.n_controlled, 1)]
-    elif policy != "replay":
-        raise ValueError(f"unknown policy {policy!r}")
+    pol = make_policy(policy, cfg, batch, seed)
+    if policy == "random":       # precomputed: the timed loop holds only the step
+        acts = [pol(t) for t in range(min(steps, 8))]
+        pol = lambda t: acts[t % len(acts)]   # noqa: E731
     torch.cuda.synchronize(dev)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
     for t in range(steps):
-        batch.step(None if acts is None else acts[t % len(acts)], auto_reset=True)
+        batch.step(pol(t), auto_reset=True)
     end.record()
     torch.cuda.synchronize(dev)
     elapsed = start.elapsed_time(end) / 1e3
@@ -656,9 +750,13 @@ class HostStepper:
         self._pending = [False] * depth
         self._t = 0
 
-    def step(self, actions) -> HostStepResult:
-        """actions: host [n_controlled, act_dim] (numpy or CPU tensor; a
-        pinned float32 tensor is copied from directly)."""
+    def step(self, actions, *, zero_copy: bool = False) -> HostStepResult:
+        """actions: host [n_controlled, act_dim] (numpy or CPU tensor).  They
+        are staged into an internal pinned buffer, so the caller may reuse
+        its own buffer as soon as step() returns.  zero_copy=True (a pinned,
+        contiguous float32 tensor only) DMAs straight from the caller's
+        buffer instead: the caller must then leave it untouched until this
+        step's HostStepResult.wait() returned."""
         b = self.batch
         k = self._t % self.depth
         a = torch.as_tensor(actions)
@@ -675,9 +773,10 @@ class HostStepper:
             # before the pinned buffers are reused (the caller has had
             # depth - 1 steps to read that result)
             self._ev_d2h[k].synchronize()
-        direct = a.dtype == torch.float32 and a.is_contiguous() and a.is_pinned()
-        src = a if direct else self._act_pin[k]
-        if not direct:
+        if zero_copy and not (a.dtype == torch.float32 and a.is_contiguous() and a.is_pinned()):
+            raise ValueError("zero_copy needs a pinned, contiguous float32 tensor")
+        src = a if zero_copy else self._act_pin[k]
+        if not zero_copy:
             src.copy_(a)
         main = torch.cuda.current_stream(b.device)
         with torch.cuda.stream(self._h2d):

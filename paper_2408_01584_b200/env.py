@@ -145,6 +145,7 @@ class VecDriveEnv:
         else:
             self.scenarios = [scenarios[w % len(scenarios)] for w in range(cfg.num_worlds)]
             self.batch = SimBatch(self.scenarios, cfg.sim, device=cfg.device)
+        self.batch.log_episodes = False   # per-step records only (env.py:103-104)
         dev = self.batch.device
         self.device = dev
         self.grid = cfg.grid
@@ -164,8 +165,15 @@ class VecDriveEnv:
         return self.batch.reset(obs_scale=self._scale)
 
     def step(self, actions):
-        """actions: (n_agents,) joint indices or (n_agents, >=2) floats."""
+        """actions: (n_agents,) joint indices or (n_agents, >=2) floats.
+        Host joint indices are range-checked here (IndexError, as the
+        reference's to_continuous); device ones by the kernel, reported by
+        SimBatch.check_status at the next episode drain."""
         a = torch.as_tensor(actions)
+        if a.ndim == 1 and a.device.type == "cpu" and a.numel():
+            n = len(self.grid.accelerations) * len(self.grid.steerings)
+            if int(a.min()) < -n or int(a.max()) >= n:
+                raise IndexError(f"joint action index outside [-{n}, {n})")
         serial = self.batch._serial
         if a.ndim == 1:
             out = self.batch.step(None, action_idx=a, grid=(self._accels, self._steers),

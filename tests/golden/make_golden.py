@@ -110,6 +110,13 @@ CONFIGS = {
     "templates_invertible_lidar": dict(dynamics="invertible", collision_behavior="ignore",
                                        obs=dict(mode="lidar", n_rays=48, max_range=40.0),
                                        scene=("templates", 3)),
+    # the reference's end-to-end acceptance scenario (test_acceptance.py:425-438):
+    # straight_road and intersection, 4 agents, seed 0, the default SimConfig
+    # with collision ignore, driven by the reference's goal_seek_actions
+    # (engine.py:559-574) rounded to float32
+    "templates_goal_seek": dict(dynamics="classic", collision_behavior="ignore",
+                                init_mode="all_nontrivial", obs=dict(mode="radial"),
+                                scene=("acceptance",), policy="goal_seek"),
 }
 FULL_OBS_STEPS = (0, 1, 91)
 # ragged batch (tests/ragged.py): hashes only, the GPU compares against the oracle
@@ -150,10 +157,20 @@ def template_scene(n_seeds: int):
     return raw_from_prepared(preps)
 
 
-def draw_actions(spec: dict, n: int, rng) -> np.ndarray:
+def acceptance_scene():
+    from drivesim.synthetic import SyntheticSpec, generate_synthetic
+    from paper_2408_01584_b200.packing import raw_from_prepared
+    return raw_from_prepared([rscn.preprocess(generate_synthetic(SyntheticSpec(t, n_agents=4, seed=0)))
+                              for t in ("straight_road", "intersection")])
+
+
+def draw_actions(spec: dict, n: int, rng, batch=None) -> np.ndarray:
     """float32-valued actions; delta_local: small ego-frame moves plus ~5 %
     of rows far outside delta_bounds (exercises the clip)."""
-    if spec["dynamics"] == "delta_local":
+    if spec.get("policy") == "goal_seek":
+        from drivesim.engine import goal_seek_actions
+        a = np.vstack([goal_seek_actions(w) for w in batch.worlds])
+    elif spec["dynamics"] == "delta_local":
         a = np.column_stack([rng.uniform(-1.0, 1.0, n), rng.uniform(-0.6, 0.6, n),
                              rng.uniform(-0.3, 0.3, n)])
         wild = rng.random(n) < 0.05
@@ -174,6 +191,8 @@ def make(name: str, spec: dict, n_worlds=3, n_agents=32, n_points=400, seed=21, 
                                        seed=seed))
         if isinstance(scene, tuple) and scene[0] == "templates":
             raw = template_scene(scene[1])
+        elif isinstance(scene, tuple) and scene[0] == "acceptance":
+            raw = acceptance_scene()
         else:
             raw = generate(WaymoSpec(**scene))
     full_obs = spec.get("full_obs", full_obs)
@@ -204,7 +223,7 @@ def make(name: str, spec: dict, n_worlds=3, n_agents=32, n_points=400, seed=21, 
     if 0 in full_obs:
         out["obs_0"] = batch.observations.copy()
     for t in range(1, steps + 1):
-        a = draw_actions(spec, n, rng)
+        a = draw_actions(spec, n, rng, batch)
         o = batch.step(a.astype(np.float64))
         acts.append(a)
         rews.append(o.rewards.copy())
@@ -223,7 +242,7 @@ def make(name: str, spec: dict, n_worlds=3, n_agents=32, n_points=400, seed=21, 
     out["poses"] = np.stack(poses)
     out["episodes"] = np.array([(e.world_id, e.n_controlled, e.n_goal, e.n_veh_collision,
                                  e.n_offroad) for e in batch.episode_infos], np.int64).reshape(-1, 5)
-    out["cfg_json"] = np.array(repr({k: v for k, v in spec.items() if k not in ("scene", "full_obs")}))
+    out["cfg_json"] = np.array(repr({k: v for k, v in spec.items() if k not in ("scene", "full_obs", "policy")}))
     path = os.path.join(HERE, f"{name}.npz")
     if os.path.exists(path):
         old = np.load(path, allow_pickle=False)

@@ -19,7 +19,7 @@ def _scenarios():
     return [scene([a, b]), scene([a, b, c])]
 
 
-@pytest.mark.parametrize("policy", ["random", "constant:1.0:0.1", "replay"])
+@pytest.mark.parametrize("policy", ["random", "constant:1.0:0.1", "replay", "goal_seek"])
 def test_benchmark_report(policy):
     cfg = SimConfig(init_mode="all_valid")
     rep = benchmark(_scenarios(), cfg, worlds=6, steps=20, policy=policy, device="cuda:0")

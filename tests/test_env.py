@@ -112,3 +112,48 @@ def test_inverted_expert_actions_reach_all_goals():
             n_ctrl += e.n_controlled
     assert n_ctrl > 0 and n_goal == n_ctrl
     env.close()
+
+
+@pytest.mark.gpu
+def test_out_of_grid_action_index_raises():
+    """to_continuous (env.py:111-116) indexes numpy arrays: a joint index in
+    [-91, 91) is valid (negative ones count from the end), anything else
+    raises IndexError -- never a silently clamped action."""
+    from paper_2408_01584_b200.env import VecDriveEnv
+    raw = generate(WaymoSpec(n_worlds=2, n_agents=8, n_points=200, seed=2, num_steps=20))
+    env = VecDriveEnv(EnvConfig(raw=raw, sim=SimConfig(obs=small_obs(), init_mode="all_valid"),
+                                device="cuda:0"))
+    env.reset()
+    n = env.n_agents
+    with pytest.raises(IndexError):
+        env.step(torch.full((n,), 91))                  # host indices: checked at once
+    with pytest.raises(IndexError):
+        env.step(np.full(n, -92))
+    env.step(torch.full((n,), -91, device="cuda:0"))    # valid: accel[-7], steer[0]
+    env.batch.check_status()
+    x0 = env.batch._x.clone()
+    env.step(torch.full((n,), 500, device="cuda:0"))    # device indices: flagged by the kernel
+    with pytest.raises(IndexError):
+        env.batch.check_status()
+    env.batch.check_status()                            # the flag was cleared
+    env.close()
+
+
+@pytest.mark.gpu
+def test_kernel_arguments_are_validated():
+    from paper_2408_01584_b200.engine import SimBatch
+    raw = generate(WaymoSpec(n_worlds=2, n_agents=8, n_points=200, seed=2))
+    cfg = SimConfig(init_mode="all_valid")
+    b = SimBatch.from_raw(raw, cfg, device="cuda:0")
+    act = torch.zeros((b.n_controlled, 2), device="cuda:0")
+    sel_w = cfg.obs.max_agents_obs + cfg.obs.max_road_points_obs
+    with pytest.raises(ValueError):          # wrong dtype
+        b.step(act, sel_idx=torch.zeros((b.n_controlled, sel_w), dtype=torch.int64, device="cuda:0"))
+    with pytest.raises(ValueError):          # too short
+        b.step(act, sel_idx=torch.zeros((1, sel_w), dtype=torch.int32, device="cuda:0"))
+    with pytest.raises(ValueError):          # host tensor
+        b.step(act, obs_scale=torch.ones(b.width))
+    with pytest.raises(ValueError):
+        b.reset(world_mask=torch.ones(1, dtype=torch.uint8, device="cuda:0"))
+    b.step(act, obs_scale=torch.ones(b.width, dtype=torch.float64, device="cuda:0"))  # converted
+    b.close()

@@ -15,8 +15,9 @@ from parity import actions_for
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("depth,pinned", [(2, True), (3, False)])
-def test_host_stepper_matches_device_step(depth, pinned):
+@pytest.mark.parametrize("depth,pinned,zero_copy", [(2, True, True), (2, True, False),
+                                                    (3, False, False)])
+def test_host_stepper_matches_device_step(depth, pinned, zero_copy):
     cfg = SimConfig(init_mode="all_valid", collision_behavior="remove_agent")
     raw = generate(WaymoSpec(n_worlds=6, n_agents=48, n_points=1500, seed=5))
     ref = SimBatch.from_raw(raw, cfg, device="cuda:0")
@@ -32,7 +33,7 @@ def test_host_stepper_matches_device_step(depth, pinned):
         out = ref.step(a.cuda(), auto_reset=True)
         want = (out.rewards.cpu().numpy(), out.dones.cpu().numpy(),
                 ref._info[:, :n].cpu().numpy())
-        got = stepper.step(a if pinned else a.numpy())
+        got = stepper.step(a if pinned else a.numpy(), zero_copy=zero_copy)
         results.append((want, got))
         if len(results) >= depth:           # read each result before its slot is reused
             (w_rew, w_done, w_info), g = results.pop(0)
@@ -50,6 +51,30 @@ def test_host_stepper_matches_device_step(depth, pinned):
     dut.close()
 
 
+def test_host_stepper_caller_may_reuse_one_buffer():
+    """The default (staged) path: the caller overwrites ONE pinned buffer with
+    the next step's actions right after step() returns, without waiting."""
+    cfg = SimConfig(init_mode="all_valid", collision_behavior="remove_agent")
+    raw = generate(WaymoSpec(n_worlds=4, n_agents=40, n_points=1200, seed=6))
+    ref = SimBatch.from_raw(raw, cfg, device="cuda:0")
+    dut = SimBatch.from_raw(raw, cfg, device="cuda:0")
+    stepper = HostStepper(dut, depth=2)
+    rng = np.random.default_rng(8)
+    buf = torch.empty((ref.n_controlled, 2), dtype=torch.float32).pin_memory()
+    for t in range(40):
+        buf.copy_(torch.from_numpy(actions_for(cfg, ref.n_controlled, rng)))
+        ref.step(buf.cuda(), auto_reset=True)
+        stepper.step(buf)
+        buf.fill_(1e3)                    # clobber it at once: must not leak into the step
+    stepper.synchronize()
+    torch.cuda.synchronize()
+    for k in ("_x", "_y", "_h", "_v", "_flags"):
+        assert torch.equal(getattr(ref, k), getattr(dut, k))
+    assert torch.equal(ref.observations, dut.observations)
+    ref.close()
+    dut.close()
+
+
 def test_host_stepper_rejects_bad_actions():
     cfg = SimConfig(init_mode="all_valid")
     raw = generate(WaymoSpec(n_worlds=2, n_agents=8, n_points=200, seed=1))
@@ -59,4 +84,6 @@ def test_host_stepper_rejects_bad_actions():
         s.step(np.zeros((b.n_controlled + 1, 2), np.float32))
     with pytest.raises(ValueError):
         s.step(torch.zeros((b.n_controlled, 2), device="cuda:0"))
+    with pytest.raises(ValueError):                  # zero_copy needs pinned float32
+        s.step(torch.zeros((b.n_controlled, 2)), zero_copy=True)
     b.close()

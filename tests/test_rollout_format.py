@@ -123,3 +123,27 @@ def test_sampler_deterministic_and_distributed(dtype):
     chi2 = float(((counts - expect) ** 2 / expect.clamp_min(1e-9))[expect > 5].sum())
     dof = int((expect > 5).sum()) - 1
     assert chi2 < dof + 6 * (2 * dof) ** 0.5
+
+
+@pytest.mark.gpu
+def test_gumbel_noise_at_the_hash_extremes():
+    """The sampler's noise is finite and accurate for every hash value,
+    including the maximum (u = 1 - 2^-24, where a naive float u would round
+    to 1 and -log(-log u) to +inf): against float64 -log(-log u)."""
+    import ctypes as C
+    from paper_2408_01584_b200 import _native as N
+    rng = np.random.default_rng(0)
+    bits = np.concatenate([np.array([0, 0x1FF, 0x200, 0xFFFFFFFF, 0xFFFFFE00, 0xFFFFFDFF,
+                                     0x80000000, 0x7FFFFFFF], np.uint32),
+                           rng.integers(0, 2**32, 4096, dtype=np.uint64).astype(np.uint32)])
+    dev_bits = torch.from_numpy(bits.view(np.int32)).cuda()
+    out = torch.empty(len(bits), dtype=torch.float32, device="cuda")
+    N.check(N.lib().ds_gumbel_noise(C.c_void_p(dev_bits.data_ptr()), len(bits),
+                                    C.c_void_p(out.data_ptr()), None), "ds_gumbel_noise")
+    got = out.cpu().numpy().astype(np.float64)
+    m = (bits >> 9).astype(np.float64)
+    u = (2 * m + 1) / 2.0**24
+    ref = -np.log(-np.log1p(-(1 - u)))
+    assert np.isfinite(got).all()
+    assert np.abs(got - ref).max() <= 4e-6 * np.maximum(1.0, np.abs(ref)).max()
+    assert got[3] == got.max() and got[3] > 16.0          # u = 1 - 2^-24: the largest noise
