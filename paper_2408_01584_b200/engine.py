@@ -223,8 +223,9 @@ class SimBatch:
     RING_STEPS = 64   # episode-ring capacity in steps of n_worlds records
 
     def __init__(self, scenarios: list, cfg: SimConfig, n_workers: int = 1,
-                 device=None, grid_cell: float | None = None, _raw: RawWorlds | None = None):
-        if _raw is None:
+                 device=None, grid_cell: float | None = None, _raw: RawWorlds | None = None,
+                 _packed: PackedWorlds | None = None):
+        if _raw is None and _packed is None:
             if not scenarios:
                 raise ValueError("need at least one scenario")
             _raw = raw_from_prepared(scenarios)
@@ -234,7 +235,7 @@ class SimBatch:
             raise ValueError("the B200 SimBatch runs on a CUDA device only (no CPU fallback)")
         if self.device.index is None:
             self.device = torch.device("cuda", torch.cuda.current_device())
-        self.packed: PackedWorlds = pack(_raw, cfg)
+        self.packed: PackedWorlds = _packed if _packed is not None else pack(_raw, cfg)
         pw = self.packed
         self.n_worlds = pw.n_worlds
         self.offsets = pw.c_off.copy()
@@ -272,6 +273,25 @@ class SimBatch:
     def from_raw(cls, raw: RawWorlds, cfg: SimConfig, device=None,
                  grid_cell: float | None = None) -> "SimBatch":
         return cls([], cfg, device=device, grid_cell=grid_cell, _raw=raw)
+
+    @classmethod
+    def from_packed(cls, packed: PackedWorlds, cfg: SimConfig, device=None,
+                    grid_cell: float | None = None) -> "SimBatch":
+        """A batch over already packed World tables (worldfile.load_packed)."""
+        return cls([], cfg, device=device, grid_cell=grid_cell, _packed=packed)
+
+    @classmethod
+    def from_file(cls, path: str, cfg: SimConfig, device=None,
+                  grid_cell: float | None = None) -> "SimBatch":
+        """A batch over a binary world file (worldfile.py): raw scenes are
+        packed, packed tables are used as they are."""
+        from . import worldfile
+        with open(path, "rb") as f:
+            hlen = worldfile._PREFIX.unpack(f.read(worldfile._PREFIX.size))[2]
+            kind = __import__("json").loads(f.read(hlen))["kind"]
+        if kind == "packed":
+            return cls.from_packed(worldfile.load_packed(path, cfg), cfg, device, grid_cell)
+        return cls.from_raw(worldfile.load_raw(path), cfg, device, grid_cell)
 
     # -- construction ------------------------------------------------------
 
