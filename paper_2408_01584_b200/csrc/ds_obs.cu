@@ -342,8 +342,13 @@ __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float be
   // phase A: rank by float key; flag near ties and possibly-out-of-radius keys
   const float r2lo = __double2float_rd(r2 - D);
   int flagged = 0;
-  for (int p = lane; p < n_g; p += 32) {
-    const float ap = S.ga()[p];
+  // warp-uniform loops (the last pass predicates its idle lanes off, the
+  // window scan runs the warp's longest window for every lane): no
+  // divergent trip counts, so no reconvergence points inside
+  for (int p0 = 0; p0 < n_g; p0 += 32) {
+    const int p = p0 + lane;
+    const bool live = p < n_g;
+    const float ap = S.ga()[live ? p : n_g - 1];
     const float t = ap * inv_w;
     const int b = min((int)t, kNB - 1);   // = bucket_of(ap, inv_w), the scatter's bucket
     const float fr = t - floorf(t);
@@ -352,21 +357,25 @@ __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float be
     const int hi = edge ? (b < bmax ? b + 1 : bmax) : b;
     const uint32_t hlo = S.hc()[lo], hhi = S.hc()[hi];
     const int start = (int)(hlo >> 16) - (int)(hlo & 0xffffu);
-    const int end = (int)(hhi >> 16);
+    const int len = live ? (int)(hhi >> 16) - start : 0;
+    const int wlen = (int)__reduce_max_sync(kFull, (unsigned)len);
     const float dlo = ap - two_d, dhi = ap + two_d;
-    // branch-free window scan; p itself lies in the window (never below dlo,
-    // always inside the band: one band count is its own)
+    // window scan; p itself lies in the window (never below dlo, always
+    // inside the band: one band count is its own)
     int rank = start, nband = 0;
-    for (int q = start; q < end; ++q) {
-      const float aq = S.ga()[q];
-      rank += aq < dlo ? 1 : 0;
-      nband += (aq >= dlo && aq <= dhi) ? 1 : 0;
+    for (int j = 0; j < wlen; ++j) {
+      const bool in = j < len;
+      const float aq = S.ga()[in ? start + j : p0];
+      rank += (in && aq < dlo) ? 1 : 0;
+      nband += (in && aq >= dlo && aq <= dhi) ? 1 : 0;
     }
     const bool amb = nband > 1;
     const uint8_t f = (amb ? 1 : 0) | (ap > r2lo ? 2 : 0) | (edge ? 8 : 0);
-    S.gf()[p] = f;
-    if (!(f & 3) && rank < k) S.sel_pl()[rank] = S.gpl()[p];
-    flagged += (f & 3) != 0;
+    if (live) {
+      S.gf()[p] = f;
+      if (!(f & 3) && rank < k) S.sel_pl()[rank] = S.gpl()[p];
+      flagged += (f & 3) != 0;
+    }
   }
   int n_invalid = 0;
   if (__any_sync(kFull, flagged)) {
@@ -451,7 +460,10 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
   double w;
   auto set_range = [&](double top) {
     r2hi = (float)(top * (1.0 + 1e-7) + 1e-30);
-    inv_w = r2hi > 0.0f ? (float)kNB / r2hi : 0.0f;
+    // any scale works here (histogram, scatter and ranking all bucket by
+    // a * inv_w; the edge bands are in those units and the window check
+    // keeps a 1 % slack on w): the fast division, no IEEE slow path
+    inv_w = r2hi > 0.0f ? __fdividef((float)kNB, r2hi) : 0.0f;
     w = (double)r2hi / kNB;
     // edge band in bucket units: twice the key error plus float slack
     beta = 2.0f * Df * inv_w + 4e-5f;
@@ -485,11 +497,13 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
       // afterwards between sorted neighbours, staged in the idle pass-1 buffer)
       const float a = lane < n ? S.ga()[lane] : INFINITY;
       const int pl = lane < n ? S.gpl()[lane] : 0x7fffffff;
-      const unsigned long long key =
-          ((unsigned long long)__float_as_uint(a) << 32) | (unsigned long long)(unsigned)pl;
-      int rank = 0;
+      // (key, payload) order = (key bits, lane): G was compacted in visit
+      // order, so payloads ascend with the lane.  One 32-bit shuffle per
+      // broadcast key; equal keys are ranked by lane with one match.
+      const unsigned ab = __float_as_uint(a);
+      int rank = __popc(__match_any_sync(kFull, ab) & ((1u << lane) - 1u));
 #pragma unroll 4
-      for (int j = 0; j < n; ++j) rank += __shfl_sync(kFull, key, j) < key ? 1 : 0;
+      for (int j = 0; j < n; ++j) rank += __shfl_sync(kFull, ab, j) < ab ? 1 : 0;
       float *const srt = S.ca();
       if (lane < n) srt[rank] = a;
       __syncwarp();
@@ -528,7 +542,9 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     __syncwarp();
     nbuf = 0;
     src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
-      if (ok) atomicAdd(&S.hc()[bucket_of(a, inv_w)], 1u);
+      // branch-free: a lane without a candidate adds 0 (its key is finite
+      // and >= 0, so its bucket index is in range)
+      atomicAdd(&S.hc()[bucket_of(a, inv_w)], ok ? 1u : 0u);
       const unsigned bal = __ballot_sync(kFull, ok);
       const int pos = nbuf + __popc(bal & ((1u << lane) - 1u));
       if (ok && pos < S.ccap) {
@@ -653,9 +669,16 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   // instead of re-reading the special registers (S2R) under register pressure
   int lane, warp;
   asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
-  asm volatile("shr.u32 %0, %1, 5;" : "=r"(warp) : "r"((int)threadIdx.x));
-  unsigned char *wb = smem_raw + WL.total * warp;
-  unsigned char *after_scratch = smem_raw + WL.total * WARPS;
+  warp = __shfl_sync(kFull, (int)threadIdx.x >> 5, 0);
+  // the dynamic shared window's base (a 32-bit shared address that depends
+  // on the CTA's cluster rank) taken once through an opaque move: otherwise
+  // the compiler rematerialises it (S2R SR_CgaCtaId + LEA) at every use
+  // under register pressure
+  uint32_t smem_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  asm volatile("mov.u32 %0, %0;" : "+r"(smem_s));
+  unsigned char *const sbase = static_cast<unsigned char *>(__cvta_shared_to_generic(smem_s));
+  unsigned char *wb = sbase + WL.total * warp;
+  unsigned char *after_scratch = sbase + WL.total * WARPS;
   float2 *pts = reinterpret_cast<float2 *>(after_scratch);
   const int amax = T.max_agents;
   double *ax = reinterpret_cast<double *>(
