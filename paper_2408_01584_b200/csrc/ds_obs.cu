@@ -31,6 +31,16 @@
 
 namespace ds {
 
+// Dev-only path counters (a build with -DDS_OBS_STATS; tools/obs_stats.py).
+#ifdef DS_OBS_STATS
+__device__ unsigned long long g_obs_stats[8];
+#define OBS_STAT(i, v) \
+  do { if (lane == 0) atomicAdd(&g_obs_stats[i], (unsigned long long)(v)); } while (0)
+#else
+#define OBS_STAT(i, v) \
+  do { } while (0)
+#endif
+
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNB = 128;       // histogram buckets
 constexpr int kCandGlobal = 640;  // buffered pass-1 candidates (global-points variant)
@@ -379,6 +389,7 @@ __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float be
   }
   int n_invalid = 0;
   if (__any_sync(kFull, flagged)) {
+    OBS_STAT(5, 1);
     __syncwarp();
     // phase B: exact (distance, id) of the flagged elements
     for (int p = lane; p < n_g; p += 32) {
@@ -471,7 +482,10 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     two_d = 2.0f * Df + 2.5e-7f * r2hi;
   };
   set_range(r2 + D);
-  if (!(beta < 0.125f)) return select_serial(src, k, radius, r2hi, S, lane);
+  if (!(beta < 0.125f)) {
+    OBS_STAT(3, 1);
+    return select_serial(src, k, radius, r2hi, S, lane);
+  }
   if (Direct) {
     int n = 0;
     src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
@@ -517,6 +531,7 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
         return n < k ? n : k;
       }
     }
+    OBS_STAT(6, 1);
     if (n <= S.gcap && n <= 0xffff) {
       if (lane == 0) S.hc()[0] = ((uint32_t)n << 16) | (uint32_t)n;
       __syncwarp();
@@ -585,7 +600,9 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     // b*+2 (all of b*+2 lies above it); edge windows are clamped to bmax
     bmax = min(bstar + 1, kNB - 1);
     // a narrowed scan is valid only if all buckets <= bmax lie inside the disc
+    OBS_STAT(1, total);
     if (restricted && !((((double)bmax + 1.01) * w + D) <= rho * rho)) {
+      OBS_STAT(2, 1);
       src.restrict_to(radius + 1e-6, lane);
       restricted = false;
       set_range(r2 + D);
@@ -612,9 +629,11 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     n_g = (hb >> 16) + (hb & 0xffffu);
   }
   if (n_g > (uint32_t)S.gcap || total > 0xffffu) {
+    OBS_STAT(3, 1);
     src.restrict_to(radius + 1e-6, lane);
     return select_serial(src, k, radius, r2hi, S, lane);
   }
+  OBS_STAT(4, n_g);
   // pass 2: counting-sort scatter of buckets <= bmax into G
   auto scatter = [&](float a, int pl) {
     const int b = bucket_of(a, inv_w);
@@ -625,8 +644,15 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     }
   };
   if (nbuf <= S.ccap && small) {
-    for (int p = lane; p < nbuf; p += 32) scatter(S.ca()[p], pb + (int)S.cp()[p]);
+    // warp-uniform trip count; idle lanes of the last pass skip the scatter
+    for (int p0 = 0; p0 < nbuf; p0 += 32) {
+      const int p = p0 + lane < nbuf ? p0 + lane : p0;
+      const float a = S.ca()[p];
+      const int pl = pb + (int)S.cp()[p];
+      if (p0 + lane < nbuf) scatter(a, pl);
+    }
   } else {
+    OBS_STAT(7, 1);
     // only keys in buckets <= bmax matter: a < (bmax + 1) w, so d^2 < that + D
     if (bmax < kNB - 1) src.restrict_to(sqrt(((double)bmax + 1.01) * w + D) + 1e-6, lane);
     src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
@@ -750,6 +776,7 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
         for (int c = lane; c < sel_w; c += 32) sel_idx[orow * sel_w + c] = -1;
       continue;
     }
+    OBS_STAT(0, 1);
     // the staged row copies the output row's 16-B phase (vector write-out)
     const int out_phase = out_row_phase(O, orow);
     float *const row = row0 - ((row0_phase - out_phase) & 3);   // contiguous staged row
@@ -785,7 +812,9 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
       slot[6] = 1.0f;
       if (sel_idx) sel_idx[orow * sel_w + m] = j;
     }
-    for (int q = 7 * ma + lane; q < 7 * cap_a; q += 32) ps[q] = 0.0f;
+    // unused partner slots read 0 (uniform trip count: 7 cap_a floats)
+    for (int q0 = 0; q0 < 7 * cap_a; q0 += 32)
+      if (q0 + lane >= 7 * ma && q0 + lane < 7 * cap_a) ps[q0 + lane] = 0.0f;
     if (sel_idx)
       for (int m = ma + lane; m < cap_a; m += 32) sel_idx[orow * sel_w + m] = -1;
     __syncwarp();
@@ -858,7 +887,8 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
         slot[1] = (float)(dy * ch - dx * sh);
         slot[2] = (float)wrap(qh - h);
 #pragma unroll
-        for (int q = 0; q < 7; ++q) slot[3 + q] = q == kind ? 1.0f : 0.0f;
+        for (int q = 0; q < 7; ++q) slot[3 + q] = 0.0f;
+        slot[3 + kind] = 1.0f;                   // road kinds are 0..6
         slot[10] = 1.0f;
         if (sel_idx) sel_idx[orow * sel_w + cap_a + m] = qid;
       } else {
@@ -873,6 +903,17 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     __syncwarp();
   }
 }
+
+#ifdef DS_OBS_STATS
+}  // namespace ds
+extern "C" int ds_debug_obs_stats(unsigned long long *out) {
+  cudaMemcpyFromSymbol(out, ds::g_obs_stats, sizeof(ds::g_obs_stats));
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(ds::g_obs_stats, z, sizeof(z));
+  return 0;
+}
+namespace ds {
+#endif
 
 cudaError_t configure_kernels(int max_dynamic_smem) {
   const void *ks[] = {(const void *)obs_radial_kernel<kWarpsShared, true, 16, 64>,

@@ -8,10 +8,10 @@ namespace ds {
 
 constexpr unsigned kFullMask = 0xffffffffu;
 
+// (int) of f clamped to [lo, hi]; f is an integral float (floorf) or a
+// bound far outside the grid, never NaN: branch-free min / max
 __device__ __forceinline__ int clampf(float f, int lo, int hi) {
-  if (f < (float)lo) return lo;
-  if (f > (float)hi) return hi;
-  return (int)f;
+  return (int)fminf(fmaxf(f, (float)lo), (float)hi);
 }
 
 // Cell rows of a query disc around (px, py) -- float coordinates relative to

@@ -12,7 +12,10 @@ b = SimBatch.from_raw(raw, cfg, device="cuda:0")
 for t in range(30):
     b.step(random_actions(b.n_controlled, cfg, 0, t, "cuda:0"), auto_reset=True)
 torch.cuda.synchronize()
+N.lib().ds_debug_obs_stats((ctypes.c_ulonglong * 8)())   # clear
+b.step(random_actions(b.n_controlled, cfg, 0, 99, "cuda:0"), auto_reset=True)
+torch.cuda.synchronize()
 out = (ctypes.c_ulonglong * 8)()
 N.lib().ds_debug_obs_stats(out)
-names = ["flagged(B/C)", "restricted", "full", "narrow_fail", "serial", "n_g>64", "nbuf>ccap", "-"]
-print({n: v for n, v in zip(names, out)}, "rows", b.n_controlled * 30)
+names = ["rows", "hist_candidates", "narrow_rerun", "serial", "sum_n_g", "flagged_BC", "partner_not_direct", "nbuf>ccap"]
+print({n: v for n, v in zip(names, out)}, "rows/step", b.n_controlled)
