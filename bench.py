@@ -146,14 +146,36 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(sm)}
 
 
-def load_traffic(config: str, kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture
-    (profiles/r1_traffic.json), or None."""
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r2_traffic.json")
+FP_PEAKS_FILE = os.path.join(ROOT, "profiles", "r2_fp_peaks.json")
+LIDAR_WORK_FILE = os.path.join(ROOT, "profiles", "r2_lidar_work.json")
+
+
+def load_json(path: str):
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-            return json.load(f)[config][kernel]
+        with open(path) as f:
+            return json.load(f)
     except Exception:
         return None
+
+
+def load_traffic(config: str, kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/r2_traffic.json, tools/ncu_traffic.py), or None."""
+    try:
+        return load_json(TRAFFIC_FILE)[config][kernel]
+    except Exception:
+        return None
+
+
+def fp_peaks() -> tuple:
+    """(FP32, FP64) FMA peaks in FLOP/s and their source: measured on a B200
+    by tools/fp_peak.cu (profiles/r2_fp_peaks.json), else derived from the SM
+    count and clock (148 SMs x 128 / 64 lanes x 2 x 1.965 GHz)."""
+    p = load_json(FP_PEAKS_FILE)
+    if p and p.get("fp32_tflops") and p.get("fp64_tflops"):
+        return p["fp32_tflops"] * 1e12, p["fp64_tflops"] * 1e12, "measured (tools/fp_peak.cu)"
+    return 74.4e12, 37.2e12, "derived (148 SMs x lanes x 2 x 1.965 GHz)"
 
 
 def load_peaks():
@@ -301,6 +323,7 @@ def parity_check(batch, raw, cfg, dev, n_worlds: int, steps: int, threads: int) 
     from paper_2408_01584_b200.engine import random_actions
     build()
     nw = min(n_worlds, batch.n_worlds)
+    OracleBatch.lidar_ties()
     ora = OracleBatch(raw.subset(range(nw)), cfg, n_threads=threads)
     rows = int(batch.offsets[nw])
     n_ag = int(batch.packed.a_off[nw])
@@ -348,6 +371,10 @@ def parity_check(batch, raw, cfg, dev, n_worlds: int, steps: int, threads: int) 
     res["max_heading_err_rad"] = float(dh.max())
     res["state_flag_mismatches"] = int((batch._flags[:n_ag].cpu().numpy().astype(np.uint16)
                                         != ora.flags[:n_ag]).sum())
+    if not radial:
+        # edge / non-edge exact-distance ties met by the oracle's rays: the
+        # one LiDAR case whose reference answer follows its BVH order
+        res["lidar_edge_ties"] = OracleBatch.lidar_ties()
     res["ok"] = (res["flag_mismatches"] == 0 and res["sel_mismatches"] == 0
                  and res["obs_out_of_tol"] == 0 and res["state_flag_mismatches"] == 0
                  and res["max_pose_err_m"] <= 1e-9 and res["max_heading_err_rad"] <= 1e-12)
@@ -636,7 +663,8 @@ def main():
     fl = radial_flops(P, A) if cfg.obs.mode == "radial" else \
         lidar_flops(leg.batch.packed, cfg.obs.max_range, cfg.obs.n_rays)
     hbm_bound = peak * 1e9 / bpa["total"]
-    fp32_bound = 74.4e12 / fl
+    fp32_peak, fp64_peak, fp_kind = fp_peaks()
+    fp32_bound = fp32_peak / fl
     roofline = None
     kernel_ms = main_leg["kernel_ms"]
     if kernel_ms is not None:
@@ -650,6 +678,21 @@ def main():
                     "algorithmic_gb_per_launch": bpa["obs_kernel"] * n / 1e9,
                     "kernel": kname,
                     "bytes_per_agent_step": bpa["obs_kernel"], "peak_kind": peak_kind}
+        if cfg.obs.mode != "radial":
+            # the LiDAR kernel's executed FP64 work: exact box / segment tests
+            # counted by the counter build on this workload (tools/lidar_work.py)
+            lw = load_json(LIDAR_WORK_FILE)
+            if lw and W == CONFIGS[args.config][0]:
+                flop = lw["executed_fp64_flop_per_agent_step"]
+                ach = flop * n / (kernel_ms["obs_kernel"] / 1e3)
+                roofline["fp64_executed"] = {
+                    "flop_per_agent_step": flop, "tests_per_agent_step": lw["per_agent_step"],
+                    "achieved_tflops": ach / 1e12, "peak_tflops": fp64_peak / 1e12,
+                    "frac": ach / fp64_peak, "peak_kind": fp_kind,
+                    "reference_candidate_flop_per_agent_step":
+                        lw["reference_candidate_flop_per_agent_step"],
+                    "note": "neither HBM nor FP64 bound: issue/latency bound on the culling "
+                            "and pair flattening (see DESIGN.md §4)"}
 
     # ---- parity episode against the oracle (rank 0, N = 1): the line's
     # parity verdict and its CPU baseline
@@ -697,7 +740,7 @@ def main():
             "roofline": roofline,
             "step_roofline": {"bytes_per_agent_step": bpa["total"],
                               "fp32_flop_per_agent_step": fl, "hbm_bound_asps": hbm_bound,
-                              "fp32_bound_asps": fp32_bound,
+                              "fp32_bound_asps": fp32_bound, "fp32_peak_kind": fp_kind,
                               "bound_asps": min(hbm_bound, fp32_bound),
                               "frac": (main_leg["value"] / world) / min(hbm_bound, fp32_bound)},
             "kernel_ms": kernel_ms,

@@ -239,6 +239,21 @@ static void radial_row(const or_tables *T, const or_config *C, const or_state *S
   }
 }
 
+/* exact-distance ties between a road edge and another road kind on a ray's
+ * nearest segment hit (see lidar_row) since the last or_lidar_ties(1) */
+static long long g_lidar_ties = 0;
+
+long long or_lidar_ties(int reset) {
+  long long v;
+#pragma omp atomic read
+  v = g_lidar_ties;
+  if (reset) {
+#pragma omp atomic write
+    g_lidar_ties = 0;
+  }
+  return v;
+}
+
 /* fill_lidar (obs:223-280) for one agent. */
 static void lidar_row(const or_tables *T, const or_config *C, const or_state *S, int w, int i,
                       double *out) {
@@ -324,6 +339,12 @@ static void lidar_row(const or_tables *T, const or_config *C, const or_state *S,
       /* nearest wins; an exact tie between a road edge and another kind goes
        * to the edge (the reference breaks such ties in BVH order) */
       const int is_edge = T->seg_kind[q] == ROAD_EDGE;
+      if (t == smin && is_edge != sedge) {
+        /* the one case where the reference's answer depends on its BVH
+         * traversal order (obs:261-271): counted, reported by or_lidar_ties */
+#pragma omp atomic
+        g_lidar_ties++;
+      }
       if (t < smin || (t == smin && is_edge && !sedge)) { smin = t; sedge = is_edge; }
     }
     if (smin < best) { best = smin; best_type = sedge ? 1 : 2; }

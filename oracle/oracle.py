@@ -76,6 +76,8 @@ def lib():
                                  _p, _p]
         for n in ("or_step", "or_reset", "or_observe"):
             getattr(L, n).restype = C.c_int
+        L.or_lidar_ties.argtypes = [C.c_int]
+        L.or_lidar_ties.restype = C.c_longlong
         _lib = L
     return _lib
 
@@ -186,6 +188,14 @@ class OracleBatch:
             "goal": self.info[0, :self.pw.n_controlled].astype(bool),
             "veh_collision": self.info[1, :self.pw.n_controlled].astype(bool),
             "offroad": self.info[2, :self.pw.n_controlled].astype(bool)}
+
+    @staticmethod
+    def lidar_ties(reset: bool = True) -> int:
+        """Exact-distance ties between a road edge and another road kind on a
+        ray's nearest segment (the only LiDAR case whose reference answer
+        depends on its BVH traversal order, observation.py:261-271) seen by
+        this process since the last reset."""
+        return int(lib().or_lidar_ties(1 if reset else 0))
 
     def observe(self):
         lib().or_observe(C.byref(self.tab), C.byref(self.ocfg), C.byref(self.st),

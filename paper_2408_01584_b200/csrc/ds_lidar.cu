@@ -28,6 +28,17 @@
 
 namespace ds {
 
+// Dev-only work counters (a build with -DDS_LIDAR_STATS; tools/lidar_work.py):
+// the executed exact tests behind the kernel's FP64 roofline.
+#ifdef DS_LIDAR_STATS
+__device__ unsigned long long g_lidar_stats[8];
+#define LIDAR_STAT(i, v) \
+  do { if (lane == 0) atomicAdd(&g_lidar_stats[i], (unsigned long long)(v)); } while (0)
+#else
+#define LIDAR_STAT(i, v) \
+  do { } while (0)
+#endif
+
 namespace {
 
 constexpr int kLidarWarps = 16;
@@ -299,6 +310,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
       zero_row(O, orow, lane);
       continue;
     }
+    LIDAR_STAT(0, 1);
     float *const row = row0 + ((out_row_phase(O, orow) - row0_phase) & 3);
     const double ox = sx[i], oy = sy[i], h = St.heading[g];
     if (lane == 0) {
@@ -354,6 +366,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
       }
       FlatRows pairs;
       pairs.build(k_lo, n_k, lane, fscr);
+      LIDAR_STAT(1, pairs.total);          // exact ray-box slab tests
       for (int p0 = 0; p0 < pairs.total; p0 += 32) {
         int owner;
         const int m = pairs.map_owner(p0, lane, owner);
@@ -436,6 +449,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
         }
         FlatRows cells;
         cells.build(sb, cnt, lane, fscr);
+        LIDAR_STAT(2, cells.total);        // segments fetched (kept cells)
+        LIDAR_STAT(4, min(32, n_cells - q0));   // cells examined
         for (int f0 = 0; f0 < cells.total; f0 += 32) {
           const int e = cells.map(f0, lane);
           int k_lo = 0, n_k = 0;
@@ -466,6 +481,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
           __syncwarp();
           FlatRows pairs;
           pairs.build(k_lo, n_k, lane, fscr);
+          LIDAR_STAT(3, pairs.total);      // exact ray-segment tests
           for (int p0 = 0; p0 < pairs.total; p0 += 32) {
             int owner;
             const int m = pairs.map_owner(p0, lane, owner);
@@ -553,3 +569,12 @@ cudaError_t launch_lidar(const ds_handle *h, const uint8_t *mask, void *obs, con
 }  // namespace ds
 
 extern "C" int ds_lidar_supported(void) { return 1; }
+
+#ifdef DS_LIDAR_STATS
+extern "C" int ds_debug_lidar_stats(unsigned long long *out) {
+  cudaMemcpyFromSymbol(out, ds::g_lidar_stats, sizeof(ds::g_lidar_stats));
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(ds::g_lidar_stats, z, sizeof(z));
+  return 0;
+}
+#endif

@@ -66,6 +66,7 @@ def run_free(case, steps=91, seed=0, raw=None, cfg=None, quantize=True):
         raw = generate(WaymoSpec(seed=seed + 11, quantize=quantize, **spec_kw))
     lidar = cfg.obs.mode != "radial"
     batch = SimBatch.from_raw(raw, cfg, device="cuda:0")
+    OracleBatch.lidar_ties()                 # reset the tie counter
     ora = OracleBatch(raw, cfg)
     n = batch.n_controlled
     sel_w = cfg.obs.max_agents_obs + cfg.obs.max_road_points_obs
@@ -92,6 +93,8 @@ def run_free(case, steps=91, seed=0, raw=None, cfg=None, quantize=True):
     eps = [(e.world_id, e.n_controlled, e.n_goal, e.n_veh_collision, e.n_offroad)
            for e in batch.episode_infos]
     assert eps == ora.episode_infos
+    # edge / non-edge exact ties (reference: BVH order; here: edge first)
+    assert OracleBatch.lidar_ties() == 0
     batch.close()
 
 
