@@ -141,6 +141,13 @@ typedef struct ds_tables {
   /* road-edge segments of eseg_* as float (ax, ay, bx, by) relative to the
    * world's grid origin, 16 B per entry: the off-road AABB prefilter */
   const float *eseg_rel;
+  /* per agent, one 32-B record (half_l, half_w, goal_x, goal_y) FP64: the
+   * step kernel's statics in one sector (length = 2 half_l and the
+   * circumradius = hypot(half_l, half_w) are exact functions of it) */
+  const double *agent_rec;
+  /* the FP64 endpoints of eseg_* as one 32-B record (ax, ay, bx, by) per
+   * entry: the off-road slab test's exact phase reads one sector */
+  const double *eseg_rec;
 } ds_tables;
 
 /* One road point of gpt_rec: the gpt_x / gpt_y / gpt_h / gpt_id / gpt_kind

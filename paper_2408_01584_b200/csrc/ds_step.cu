@@ -155,7 +155,10 @@ __device__ bool offroad_query(const ds_tables &T, const ds_config &C, int w, dou
             fmaxf(q[u].y, q[u].w) < fcy - fry || fminf(q[u].y, q[u].w) > fcy + fry)
           continue;
         const int k = k0 + u;
-        const double ax = T.eseg_ax[k], ay = T.eseg_ay[k], bx = T.eseg_bx[k], by = T.eseg_by[k];
+        // FP64 endpoints: one 32-B record (one sector) per entry
+        const double2 *er = reinterpret_cast<const double2 *>(T.eseg_rec) + 2 * (int64_t)k;
+        const double2 e0 = er[0], e1 = er[1];
+        const double ax = e0.x, ay = e0.y, bx = e1.x, by = e1.y;
         // segment AABB vs box AABB (with slack): a superset prefilter
         if (fmax(ax, bx) < cx - rx || fmin(ax, bx) > cx + rx || fmax(ay, by) < cy - ry ||
             fmin(ay, by) > cy + ry)
@@ -227,6 +230,14 @@ __global__ void __launch_bounds__(MAXT, MINB) step_kernel(ds_tables T, ds_config
 
   uint16_t f = 0;
   double x = 0, y = 0, h = 0, v = 0;
+  // statics, one 32-B record: half-extents and goal (length = 2 half_l and
+  // the circumradius hypot(half_l, half_w) are exact functions of them)
+  double2 st_hlw = make_double2(0.0, 0.0), st_goal = make_double2(0.0, 0.0);
+  if (act_here) {
+    const double2 *ar = reinterpret_cast<const double2 *>(T.agent_rec) + 2 * g;
+    st_hlw = ar[0];
+    st_goal = ar[1];
+  }
   if (act_here) {
     f = S.flags[g];
     // (1) remove agents flagged last step (engine.py:379-380)
@@ -265,7 +276,7 @@ __global__ void __launch_bounds__(MAXT, MINB) step_kernel(ds_tables T, ds_config
           a1v = a.grid_steer[si];
         }
       }
-      const double L = T.length[g];
+      const double L = 2.0 * st_hlw.x;   // == length exactly (half_l = 0.5 length)
       if (bad_action) {
         // pose held (the reference would have raised before stepping)
       } else if (C.dynamics == DS_DYN_CLASSIC) {
@@ -324,16 +335,18 @@ __global__ void __launch_bounds__(MAXT, MINB) step_kernel(ds_tables T, ds_config
     sh.y[tid] = y;
     sh.c[tid] = cos(h);
     sh.s[tid] = sin(h);
-    sh.hl[tid] = T.half_l[g];
-    sh.hw[tid] = T.half_w[g];
-    sh.cr[tid] = T.circumradius[g];
+    // np.hypot(half_l, half_w) (engine.py:189): the glibc-exact port
+    const double cr = hypot(st_hlw.x, st_hlw.y);
+    sh.hl[tid] = st_hlw.x;
+    sh.hw[tid] = st_hlw.y;
+    sh.cr[tid] = cr;
     const bool elig = (f & DS_F_PRESENT) && !(f & DS_F_REMOVED) &&
                       ((ctrl && !(f & DS_F_DONE)) || T.rep_valid[rn]);
     sh.elig[tid] = elig;
     // |fx - (x - x0)| <= 2^-24 |x - x0|: pad the radius by 2.4e-7 (|fx| + |fy|)
     // + 1 mm, so that float distances > the padded sum prove disjoint circles
     const float fx = (float)(x - T.grid_x0[w]), fy = (float)(y - T.grid_y0[w]);
-    const float pr = (float)T.circumradius[g] * (1.0f + 1e-6f) + 1e-3f +
+    const float pr = (float)cr * (1.0f + 1e-6f) + 1e-3f +
                      2.4e-7f * (fabsf(fx) + fabsf(fy));
     sh.pre[tid] = make_float4(fx, fy, pr, elig ? 1.0f : 0.0f);
     sh.hit[tid] = 0;
@@ -413,8 +426,8 @@ __global__ void __launch_bounds__(MAXT, MINB) step_kernel(ds_tables T, ds_config
   if (n_rows > 0 && act_here) {
     live = ctrl && !(f & (DS_F_REMOVED | DS_F_DONE));
     if (live) {
-      const double dgx = x - T.goal_x[g];
-      const double dgy = y - T.goal_y[g];
+      const double dgx = x - st_goal.x;
+      const double dgy = y - st_goal.y;
       at_goal = hypot(dgx, dgy) <= C.goal_tolerance;
     }
     if (at_goal) f |= DS_F_GOAL_REACHED | DS_F_GOAL_EVER | DS_F_PENDING | DS_F_DONE;
@@ -527,8 +540,12 @@ cudaError_t launch_goal_seek(const ds_handle *h, float *out, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+#ifndef DS_STEP_MINB
+#define DS_STEP_MINB 8   // CTAs (x 4 warps) per SM of the <= 128-agent variant
+#endif
+
 cudaError_t configure_step_kernels(int max_dynamic_smem) {
-  const void *ks[] = {(const void *)step_kernel<128, 8>, (const void *)step_kernel<256, 1>,
+  const void *ks[] = {(const void *)step_kernel<128, DS_STEP_MINB>, (const void *)step_kernel<256, 1>,
                       (const void *)step_kernel<1024, 1>};
   for (const void *k : ks) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -540,7 +557,7 @@ cudaError_t configure_step_kernels(int max_dynamic_smem) {
 
 cudaError_t launch_step(const ds_handle *h, const ds_step_args *a, cudaStream_t s) {
   if (h->step_threads <= 128)   // 8 CTAs (32 warps) per SM at <= 64 registers
-    step_kernel<128, 8><<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg,
+    step_kernel<128, DS_STEP_MINB><<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg,
                                                                               h->st, *a);
   else if (h->step_threads <= 256)
     step_kernel<256, 1><<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg,

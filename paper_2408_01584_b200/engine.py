@@ -323,6 +323,11 @@ class SimBatch:
             rec["x"], rec["y"], rec["h"] = lay.gpt_x, lay.gpt_y, lay.gpt_h
             rec["id"], rec["kind"] = lay.gpt_id, lay.gpt_kind
         t["gpt_rec"] = torch.from_numpy(rec.view(np.uint8)).to(dev)
+        # 32-B per-agent statics and FP64 edge-segment records (step kernel)
+        t["agent_rec"] = _dev(np.stack([pw.half_l, pw.half_w, pw.goal_x, pw.goal_y], 1)
+                              .astype(np.float64).reshape(-1), dev)
+        t["eseg_rec"] = _dev(np.stack([lay.eseg_ax, lay.eseg_ay, lay.eseg_bx, lay.eseg_by], 1)
+                             .astype(np.float64).reshape(-1), dev)
         t["p_off"] = _dev(pw.p_off, dev)
         t["s_off"] = _dev(pw.s_off, dev)
         self._t_tensors = t
