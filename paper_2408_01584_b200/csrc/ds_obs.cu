@@ -56,6 +56,7 @@ constexpr int kWarpsSharedSmall = 24;
 constexpr int kWarpsSharedPair = 16;
 constexpr int kSmemPerSM = 228 * 1024;
 constexpr int kWarpsGlobal = 12;
+constexpr size_t kStaticSmem = 16;   // the points' mbarrier (static shared memory)
 
 __host__ __device__ constexpr int kmax_of(int cap_a, int cap_r) {
   return (cap_a > cap_r ? cap_a : cap_r) < 1 ? 1 : (cap_a > cap_r ? cap_a : cap_r);
@@ -74,7 +75,7 @@ __host__ __device__ constexpr size_t al16(size_t v) { return (v + 15) & ~size_t(
 // selection has produced sel_pl.  constexpr: with compile-time slot caps the
 // whole layout folds into immediate offsets off one base register.
 struct WarpLayout {
-  size_t row, hc, ca, cp, ga, ge, gid, gpl, gf, sel_pl, fr, total;
+  size_t row, hc, ca, cp, ga, ge, gid, gpl, gf, road_end, sel_pl, psel, fr, total;
 };
 
 __host__ __device__ constexpr WarpLayout make_layout(int cap_a, int cap_r, bool buffered) {
@@ -107,8 +108,10 @@ __host__ __device__ constexpr WarpLayout make_layout(int cap_a, int cap_r, bool 
   L.gpl = o; o = al16(o + gc * sizeof(int));
   L.gf = o; o = al16(o + gc);
   const size_t road_end = al16(L.hc + (size_t)cap_r * 11 * sizeof(float));
+  L.road_end = road_end;
   if (o < road_end) o = road_end;
   L.sel_pl = o; o = al16(o + km * sizeof(int));
+  L.psel = o; o = al16(o + (cap_a > 0 ? cap_a : 1) * sizeof(int));   // partner picks
   L.fr = o; o = al16(o + 32 * sizeof(int));   // FlatRows compaction scratch
   L.total = o;
   return L;
@@ -118,15 +121,45 @@ __host__ __device__ inline WarpLayout warp_layout(const ds_config &c, bool buffe
   return make_layout(c.max_agents_obs, c.max_road_points_obs, buffered);
 }
 
-// per agent: x, y, heading, speed, length, width, cos, sin (f64) + visible (u8)
-// + per row: the agent's local index and flags (row loop header from shared)
-__host__ __device__ inline size_t agents_bytes(int max_agents) {
-  return al16((size_t)max_agents * (8 * sizeof(double) + 1)) +
-         al16((size_t)max_agents * (sizeof(uint16_t) + sizeof(uint16_t)));
+// Per-agent tables staged once per world (structure of arrays):
+//   x, y, heading, speed, length, width, cos, sin (f64) | search hint (float4)
+//   | ego block (7 floats, padded to 8) | flags (u16) | visible (u8)
+//   | row -> local agent (u16)
+struct AgentTabs {
+  double *x, *y, *h, *v, *l, *w, *c, *s;
+  float4 *hint;
+  float *ego;
+  uint16_t *flg, *rloc;
+  uint8_t *vis;
+};
+
+__host__ __device__ inline size_t agents_bytes(int amax) {
+  return (size_t)amax * (8 * sizeof(double) + sizeof(float4) + 8 * sizeof(float)) +
+         al16((size_t)amax * sizeof(uint16_t)) * 2 + al16((size_t)amax);
+}
+
+__device__ inline AgentTabs agent_tabs(unsigned char *base, int amax) {
+  AgentTabs t;
+  double *d = reinterpret_cast<double *>(base);
+  t.x = d; t.y = d + amax; t.h = d + 2 * amax; t.v = d + 3 * amax;
+  t.l = d + 4 * amax; t.w = d + 5 * amax; t.c = d + 6 * amax; t.s = d + 7 * amax;
+  unsigned char *o = base + (size_t)amax * 8 * sizeof(double);
+  t.hint = reinterpret_cast<float4 *>(o); o += (size_t)amax * sizeof(float4);
+  t.ego = reinterpret_cast<float *>(o); o += (size_t)amax * 8 * sizeof(float);
+  t.flg = reinterpret_cast<uint16_t *>(o); o += al16((size_t)amax * sizeof(uint16_t));
+  t.rloc = reinterpret_cast<uint16_t *>(o); o += al16((size_t)amax * sizeof(uint16_t));
+  t.vis = o;
+  return t;
+}
+
+// road points: float2, +2 entries of slack so the bulk copy's 16-B aligned
+// body can start at an odd point offset
+__host__ __device__ inline size_t points_bytes(int max_points) {
+  return al16((size_t)(max_points + 2) * sizeof(float2));
 }
 
 size_t obs_smem_bytes_shared(const ds_config &cfg, int max_agents, int max_points, int warps) {
-  return agents_bytes(max_agents) + al16((size_t)max_points * sizeof(float2)) +
+  return agents_bytes(max_agents) + points_bytes(max_points) +
          warp_layout(cfg, false).total * warps;
 }
 
@@ -158,6 +191,49 @@ __device__ __forceinline__ bool key_less(double da, int ia, double db, int ib) {
 __device__ __forceinline__ int bucket_of(float a, float inv_w) {
   const int b = (int)(a * inv_w);
   return b < kNB ? b : kNB - 1;
+}
+
+// Asynchronous copies.  The world's road points arrive by one bulk copy (TMA
+// engine, completion counted on an mbarrier) while the threads stage the
+// agent tables; the selected road-point records of a row are fetched with
+// 16-B cp.async into dead scratch while the partner slots are formed.
+__device__ __forceinline__ uint32_t sm_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(sm_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// global -> shared bulk copy (16-B aligned addresses, size a multiple of 16)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          sm_addr(dst)),
+      "l"(src), "r"(bytes), "r"(sm_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sm_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -681,16 +757,22 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     const float *scale, int32_t *sel_idx, int obs_width) {
   const int w = blockIdx.x;
   if (mask && !mask[w]) return;
-  const int64_t c0 = T.c_off[w];
-  const int nrow = (int)(T.c_off[w + 1] - c0);
+  // every per-world offset in one round of independent loads
+  const int64_t c0 = T.c_off[w], c1 = T.c_off[w + 1];
+  const int64_t a0 = T.a_off[w], a1 = T.a_off[w + 1];
+  const int64_t p0 = T.p_off[w], p1 = T.p_off[w + 1];
+  const int nrow = (int)(c1 - c0);
   if (nrow == 0) return;
+  const int A = (int)(a1 - a0);
+  const int np = (int)(p1 - p0);
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint64_t pts_bar;
   constexpr bool kFixed = CAPA > 0;
   const int cap_a = kFixed ? CAPA : C.max_agents_obs, cap_r = kFixed ? CAPR : C.max_road_points_obs;
   constexpr WarpLayout kWL = make_layout(CAPA, CAPR, !SharedPts);
   const WarpLayout WL = kFixed ? kWL : warp_layout(C, !SharedPts);
-  // shared memory: [per-warp scratch x WARPS][road points][agents] -- the
-  // scratch and the points sit at (compile-time) constant offsets
+  // shared memory: [per-warp scratch x WARPS][road points][agent tables] --
+  // the scratch and the points sit at (compile-time) constant offsets
   // lane / warp from opaque moves: the compiler keeps them in registers
   // instead of re-reading the special registers (S2R) under register pressure
   int lane, warp;
@@ -705,15 +787,30 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   unsigned char *const sbase = static_cast<unsigned char *>(__cvta_shared_to_generic(smem_s));
   unsigned char *wb = sbase + WL.total * warp;
   unsigned char *after_scratch = sbase + WL.total * WARPS;
-  float2 *pts = reinterpret_cast<float2 *>(after_scratch);
   const int amax = T.max_agents;
-  double *ax = reinterpret_cast<double *>(
-      after_scratch + (SharedPts ? al16((size_t)T.max_points * sizeof(float2)) : 0));
-  double *ay = ax + amax, *ah = ax + 2 * amax, *av = ax + 3 * amax, *al = ax + 4 * amax,
-         *aw = ax + 5 * amax, *ac = ax + 6 * amax, *as = ax + 7 * amax;
-  uint8_t *avis = reinterpret_cast<uint8_t *>(ax + 8 * amax);
-  const int64_t p0 = T.p_off[w];
-  const int np = (int)(T.p_off[w + 1] - p0);
+  // points: the 16-B aligned body [pa, pb) of the world's range by one bulk
+  // copy, an odd head / tail point by plain loads; pts[j] = point p0 + j
+  float2 *const pbuf = reinterpret_cast<float2 *>(after_scratch);
+  float2 *const pts = pbuf + (p0 & 1);
+  if (SharedPts && threadIdx.x == 0) {
+    mbar_init(&pts_bar, 1);
+    const int64_t pa = (p0 + 1) & ~int64_t(1), pb = p1 & ~int64_t(1);
+    const float2 *src = reinterpret_cast<const float2 *>(T.gpt_xy);
+    if (pb > pa) {
+      const uint32_t bytes = (uint32_t)((pb - pa) * sizeof(float2));
+      mbar_arrive_tx(&pts_bar, bytes);
+      bulk_g2s(pbuf + (pa - (p0 & ~int64_t(1))), src + pa, bytes, &pts_bar);
+    } else {
+      mbar_arrive(&pts_bar);
+    }
+  }
+  if (SharedPts && threadIdx.x == 32) {
+    const float2 *src = reinterpret_cast<const float2 *>(T.gpt_xy);
+    const int64_t pa = (p0 + 1) & ~int64_t(1), pb = p1 & ~int64_t(1);
+    if (p0 < pa && p0 < p1) pts[0] = src[p0];
+    if (pb < p1 && pb >= pa) pts[pb - p0] = src[pb];
+  }
+  const AgentTabs AT = agent_tabs(after_scratch + (SharedPts ? points_bytes(T.max_points) : 0), amax);
   Sel S;
   S.wb = wb;
   S.L = WL;
@@ -722,36 +819,33 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   float *const row0 = reinterpret_cast<float *>(wb + WL.row);
   const int row0_phase = (int)((reinterpret_cast<uintptr_t>(row0) >> 2) & 3);
 
-  const int64_t a0 = T.a_off[w];
-  const int A = (int)(T.a_off[w + 1] - a0);
+  // agent tables, the ego block of every agent (fp:228-238) and the search
+  // hints: one thread per agent, overlapping the points' bulk copy
   for (int i = threadIdx.x; i < A; i += blockDim.x) {
     const int64_t g = a0 + i;
-    ax[i] = St.x[g];
-    ay[i] = St.y[g];
-    const double hd = St.heading[g];
-    ah[i] = hd;
-    sincos(hd, &as[i], &ac[i]);
-    av[i] = St.speed[g];
-    al[i] = T.length[g];
-    aw[i] = T.width[g];
+    const double px = St.x[g], py = St.y[g], hd = St.heading[g], v = St.speed[g];
+    const double ln = T.length[g], wd = T.width[g];
+    const double gx = T.goal_x[g] - px, gy = T.goal_y[g] - py;
     const uint16_t f = St.flags[g];
-    avis[i] = (f & DS_F_PRESENT) && !(f & DS_F_REMOVED);
+    AT.hint[i] = St.obs_hint ? reinterpret_cast<const float4 *>(St.obs_hint)[g]
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+    double sh, ch;
+    sincos(hd, &sh, &ch);
+    AT.x[i] = px; AT.y[i] = py; AT.h[i] = hd; AT.v[i] = v;
+    AT.l[i] = ln; AT.w[i] = wd; AT.c[i] = ch; AT.s[i] = sh;
+    AT.flg[i] = f;
+    AT.vis[i] = (f & DS_F_PRESENT) && !(f & DS_F_REMOVED);
+    float *e = AT.ego + 8 * i;
+    e[0] = (float)v;
+    e[1] = (float)ln;
+    e[2] = (float)wd;
+    e[3] = (float)(gx * ch + gy * sh);
+    e[4] = (float)(gy * ch - gx * sh);
+    e[5] = (float)hypot(gx, gy);
+    e[6] = (f & DS_F_COLLIDED) ? 1.0f : 0.0f;
   }
-  // row -> (local agent, flags), so the row loop starts from shared memory
-  uint16_t *rloc = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(ax) +
-                                                al16((size_t)amax * (8 * sizeof(double) + 1)));
-  uint16_t *rflg = rloc + amax;
-  for (int r = threadIdx.x; r < nrow; r += blockDim.x) {
-    const int64_t g = T.row_agent[c0 + r];
-    rloc[r] = (uint16_t)(g - a0);
-    rflg[r] = St.flags[g];
-  }
-  if (SharedPts) {
-    const float2 *src = reinterpret_cast<const float2 *>(T.gpt_xy) + p0;
-    for (int j = threadIdx.x; j < np; j += blockDim.x) pts[j] = src[j];
-  }
-  __syncthreads();
-
+  // row -> local agent, so the row loop starts from shared memory
+  for (int r = threadIdx.x; r < nrow; r += blockDim.x) AT.rloc[r] = (uint16_t)(T.row_agent[c0 + r] - a0);
   const double radius = K.radius;
   const double reach = K.reach;         // culling slack; membership is decided exactly
   const int road_off = 7 + 7 * cap_a;
@@ -762,12 +856,16 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   const int64_t cbase = T.grid_cell_off[w];
   const double eps_p = SharedPts ? T.grid_eps[w] : 0.0;
   const double D_fp64 = K.D_fp64;       // fl32 of an FP64 d^2
+  __syncthreads();
+  if (SharedPts) mbar_wait(&pts_bar, 0);
+  const double *ax = AT.x, *ay = AT.y, *ah = AT.h, *av = AT.v, *al = AT.l, *aw = AT.w, *ac = AT.c,
+               *as = AT.s;
 
   for (int r = warp; r < nrow; r += WARPS) {
     const int64_t orow = c0 + r;
-    const int i = rloc[r];
+    const int i = AT.rloc[r];
     const int64_t g = a0 + i;
-    const uint16_t f = rflg[r];
+    const uint16_t f = AT.flg[i];
     if (f & (DS_F_DONE | DS_F_REMOVED)) {
       // finished / removed rows are zero-filled (engine.py:502-512)
       zero_row(O, orow, lane);
@@ -782,48 +880,21 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     float *const row = row0 - ((row0_phase - out_phase) & 3);   // contiguous staged row
     const double px = ax[i], py = ay[i], h = ah[i];
     const double ch = ac[i], sh = as[i];
-    if (lane == 0) {
-      // ego block (fp:228-238)
-      const double gx = T.goal_x[g] - px, gy = T.goal_y[g] - py;
-      row[0] = (float)av[i];
-      row[1] = (float)al[i];
-      row[2] = (float)aw[i];
-      row[3] = (float)(gx * ch + gy * sh);
-      row[4] = (float)(gy * ch - gx * sh);
-      row[5] = (float)hypot(gx, gy);
-      row[6] = (f & DS_F_COLLIDED) ? 1.0f : 0.0f;
-    }
+    if (lane < 7) row[lane] = AT.ego[8 * i + lane];   // ego block, formed in the prologue
 
-    // ---- partners
-    PartnerSrc psrc{ax, ay, avis, A, i, px, py};
+    // ---- partners: the picks are kept aside (psel); their slots are formed
+    // while the selected road records are in flight
+    PartnerSrc psrc{ax, ay, AT.vis, A, i, px, py};
     float no_bound = 0.0f;
     const int ma = select_topk<true>(psrc, cap_a, radius, D_fp64, S, lane, radius, no_bound);
-    float *ps = row + 7;
-    for (int m = lane; m < ma; m += 32) {
-      const int j = S.sel_pl()[m];
-      const double dx = ax[j] - px, dy = ay[j] - py;
-      float *slot = ps + 7 * m;
-      slot[0] = (float)(dx * ch + dy * sh);
-      slot[1] = (float)(dy * ch - dx * sh);
-      slot[2] = (float)wrap(ah[j] - h);
-      slot[3] = (float)(av[j] - av[i]);
-      slot[4] = (float)al[j];
-      slot[5] = (float)aw[j];
-      slot[6] = 1.0f;
-      if (sel_idx) sel_idx[orow * sel_w + m] = j;
-    }
-    // unused partner slots read 0 (uniform trip count: 7 cap_a floats)
-    for (int q0 = 0; q0 < 7 * cap_a; q0 += 32)
-      if (q0 + lane >= 7 * ma && q0 + lane < 7 * cap_a) ps[q0 + lane] = 0.0f;
-    if (sel_idx)
-      for (int m = ma + lane; m < cap_a; m += 32) sel_idx[orow * sel_w + m] = -1;
+    int *const psel = reinterpret_cast<int *>(wb + WL.psel);
+    for (int m = lane; m < ma; m += 32) psel[m] = S.sel_pl()[m];
     __syncwarp();
 
     // ---- road points: lane l owns cell row iy0 + l of the disc
     int mr = 0;
     // search hint: (bound on the k-th road distance, position it was taken at)
-    float4 hint = St.obs_hint ? reinterpret_cast<const float4 *>(St.obs_hint)[g]
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 hint = AT.hint[i];
     float bound = 0.0f;
     // bound on this step's k-th distance: the hint plus the distance moved
     // (float; the 1 mm slack exceeds the rounding of the grid-relative floats)
@@ -857,44 +928,86 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     if (St.obs_hint && lane == 0)
       reinterpret_cast<float4 *>(St.obs_hint)[g] =
           make_float4(bound, (float)(px - gx0), (float)(py - gy0), 0.0f);
-    // road block staged as the final 11-float slots (aliases the dead scratch)
+    // the selected records (32 B, one sector each) are fetched into the dead
+    // selection scratch at the END of the road block ([road_end - 32 cap_r,
+    // road_end)): the slots of batch u (44 B each, written from the start)
+    // never reach the records of batch u + 1.  Each lane fetches the records
+    // of the slots it forms.
     float *rstage = row + road_off;
+    const double2 *recs = reinterpret_cast<const double2 *>(wb + WL.road_end) - 2 * cap_r;
     const int sel_off = SharedPts ? (int)p0 : 0;
-    for (int m = lane; m < cap_r; m += 32) {
-      float *slot = rstage + 11 * m;
+    if (SharedPts) {
+      const double2 *grec = reinterpret_cast<const double2 *>(T.gpt_rec);
+      for (int m = lane; m < mr; m += 32) {
+        const int64_t s2 = 2 * (int64_t)(S.sel_pl()[m] + sel_off);
+        cp_async16(const_cast<double2 *>(recs + 2 * m), grec + s2);
+        cp_async16(const_cast<double2 *>(recs + 2 * m + 1), grec + s2 + 1);
+      }
+    }
+
+    // ---- partner slots (fp:240-272) while the records arrive
+    float *ps = row + 7;
+    for (int m = lane; m < ma; m += 32) {
+      const int j = psel[m];
+      const double dx = ax[j] - px, dy = ay[j] - py;
+      float *slot = ps + 7 * m;
+      slot[0] = (float)(dx * ch + dy * sh);
+      slot[1] = (float)(dy * ch - dx * sh);
+      slot[2] = (float)wrap(ah[j] - h);
+      slot[3] = (float)(av[j] - av[i]);
+      slot[4] = (float)al[j];
+      slot[5] = (float)aw[j];
+      slot[6] = 1.0f;
+      if (sel_idx) sel_idx[orow * sel_w + m] = j;
+    }
+    // unused partner slots read 0 (uniform trip count: 7 cap_a floats)
+    for (int q0 = 0; q0 < 7 * cap_a; q0 += 32)
+      if (q0 + lane >= 7 * ma && q0 + lane < 7 * cap_a) ps[q0 + lane] = 0.0f;
+    if (sel_idx)
+      for (int m = ma + lane; m < cap_a; m += 32) sel_idx[orow * sel_w + m] = -1;
+
+    // ---- road slots (fp:274-300), 32 per batch: read the batch's records,
+    // sync, then overwrite the scratch with the slots
+    if (SharedPts) cp_async_wait_all();
+    for (int m0 = 0; m0 < cap_r; m0 += 32) {
+      const int m = m0 + lane;
+      double qx = 0.0, qy = 0.0, qh = 0.0;
+      int qid = 0, kind = 0;
       if (m < mr) {
-        const int s = S.sel_pl()[m] + sel_off;
-        double qx, qy, qh;
-        int kind, qid;
         if (SharedPts) {
-          // one 32-B record (ds_point_rec): two 16-B loads of one sector
-          const double2 *r2 = reinterpret_cast<const double2 *>(T.gpt_rec) + 2 * (int64_t)s;
-          const double2 a = r2[0], b = r2[1];
-          qx = a.x;
-          qy = a.y;
-          qh = b.x;
-          qid = __double2loint(b.y);
-          kind = (int)(signed char)(__double2hiint(b.y) & 0xff);
+          const double2 ra = recs[2 * m], rb = recs[2 * m + 1];
+          qx = ra.x;
+          qy = ra.y;
+          qh = rb.x;
+          qid = __double2loint(rb.y);
+          kind = (int)(signed char)(__double2hiint(rb.y) & 0xff);
         } else {
+          const int s = S.sel_pl()[m];
           qx = T.gpt_x[s];
           qy = T.gpt_y[s];
           qh = T.gpt_h[s];
           kind = T.gpt_kind[s];
           qid = T.gpt_id[s];
         }
-        const double dx = qx - px, dy = qy - py;
-        slot[0] = (float)(dx * ch + dy * sh);
-        slot[1] = (float)(dy * ch - dx * sh);
-        slot[2] = (float)wrap(qh - h);
+      }
+      __syncwarp();
+      if (m < cap_r) {
+        float *slot = rstage + 11 * m;
+        if (m < mr) {
+          const double dx = qx - px, dy = qy - py;
+          slot[0] = (float)(dx * ch + dy * sh);
+          slot[1] = (float)(dy * ch - dx * sh);
+          slot[2] = (float)wrap(qh - h);
 #pragma unroll
-        for (int q = 0; q < 7; ++q) slot[3 + q] = 0.0f;
-        slot[3 + kind] = 1.0f;                   // road kinds are 0..6
-        slot[10] = 1.0f;
-        if (sel_idx) sel_idx[orow * sel_w + cap_a + m] = qid;
-      } else {
+          for (int q = 0; q < 7; ++q) slot[3 + q] = 0.0f;
+          slot[3 + kind] = 1.0f;                   // road kinds are 0..6
+          slot[10] = 1.0f;
+          if (sel_idx) sel_idx[orow * sel_w + cap_a + m] = qid;
+        } else {
 #pragma unroll
-        for (int q = 0; q < 11; ++q) slot[q] = 0.0f;
-        if (sel_idx) sel_idx[orow * sel_w + cap_a + m] = -1;
+          for (int q = 0; q < 11; ++q) slot[q] = 0.0f;
+          if (sel_idx) sel_idx[orow * sel_w + cap_a + m] = -1;
+        }
       }
     }
     __syncwarp();
@@ -925,8 +1038,13 @@ cudaError_t configure_kernels(int max_dynamic_smem) {
                       (const void *)obs_radial_kernel<kWarpsGlobal, false, 16, 64>,
                       (const void *)obs_radial_kernel<kWarpsGlobal, false, 0, 0>};
   for (const void *k : ks) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         max_dynamic_smem);
+    // the opt-in limit covers static + dynamic shared memory (the points'
+    // mbarrier is static)
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             max_dynamic_smem - (int)fa.sharedSizeBytes);
     if (e != cudaSuccess) return e;
   }
   cudaError_t e = configure_lidar_kernels(max_dynamic_smem);
@@ -952,11 +1070,11 @@ void obs_plan(ds_handle *h, int max_optin) {
     h->obs_shared_pts = 1;
     h->obs_warps = kWarpsSharedPair;
     h->obs_smem = sh_pair;
-  } else if (can && sh <= (size_t)max_optin) {
+  } else if (can && sh + kStaticSmem <= (size_t)max_optin) {
     h->obs_shared_pts = 1;
     h->obs_warps = kWarpsShared;
     h->obs_smem = sh;
-  } else if (can && sh_small <= (size_t)max_optin) {
+  } else if (can && sh_small + kStaticSmem <= (size_t)max_optin) {
     h->obs_shared_pts = 1;
     h->obs_warps = kWarpsSharedSmall;
     h->obs_smem = sh_small;
