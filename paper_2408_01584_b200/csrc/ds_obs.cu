@@ -74,8 +74,13 @@ __host__ __device__ constexpr size_t al16(size_t v) { return (v + 15) & ~size_t(
 // block (11 floats per slot) aliases [hc ..), which is dead once the road
 // selection has produced sel_pl.  constexpr: with compile-time slot caps the
 // whole layout folds into immediate offsets off one base register.
+//   R1 = the pass-1 candidate buffer (ca keys, cp payloads), dead once
+//        scattered into G; then the sorted G (sa keys, spl payloads) and the
+//        exact ids sid
+//   R2 = G in bucket order (ga keys, gpl payloads), dead once sorted; then
+//        the exact distances se of the sorted G
 struct WarpLayout {
-  size_t row, hc, ca, cp, ga, ge, gid, gpl, gf, road_end, sel_pl, psel, fr, total;
+  size_t row, hc, ca, cp, sa, spl, sid, ga, gpl, se, sf, road_end, sel_pl, psel, fr, total;
 };
 
 __host__ __device__ constexpr WarpLayout make_layout(int cap_a, int cap_r, bool buffered) {
@@ -88,25 +93,19 @@ __host__ __device__ constexpr WarpLayout make_layout(int cap_a, int cap_r, bool 
   L.row = o - head;
   L.hc = o; o = al16(o + kNB * sizeof(uint32_t));
   const int cc = buffered ? kCandGlobal : kCandShared;
-  // the buffered pass-1 candidates (ca, cp) are dead once pass 2 has
-  // scattered them into G; the exact distances ge of G alias them
+  const size_t g4 = al16((size_t)gc * 4);
   L.ca = o;
-  L.ge = o;
-  const size_t cand_end = al16(al16(o + cc * sizeof(float)) + cc * sizeof(uint16_t));
   L.cp = al16(o + cc * sizeof(float));
-  const size_t ge_end = al16(o + gc * sizeof(double));
-  o = cand_end > ge_end ? cand_end : ge_end;
-  // the exact ids gid of G (phase B on) alias the pass-1 payloads cp (dead
-  // once scattered) when they fit beside ge
-  const bool gid_in_cp = ge_end <= L.cp && (size_t)gc * sizeof(int) <= (size_t)cc * sizeof(uint16_t);
-  L.ga = o; o = al16(o + gc * sizeof(float));
-  if (gid_in_cp) {
-    L.gid = L.cp;
-  } else {
-    L.gid = o; o = al16(o + gc * sizeof(int));
-  }
-  L.gpl = o; o = al16(o + gc * sizeof(int));
-  L.gf = o; o = al16(o + gc);
+  const size_t cand_end = al16(L.cp + cc * sizeof(uint16_t));
+  L.sa = o;
+  L.spl = o + g4;
+  L.sid = o + 2 * g4;
+  o = cand_end > o + 3 * g4 ? cand_end : o + 3 * g4;
+  L.ga = o;
+  L.gpl = o + g4;
+  L.se = o;
+  o = o + 2 * g4 > al16(o + (size_t)gc * sizeof(double)) ? o + 2 * g4 : al16(o + (size_t)gc * sizeof(double));
+  L.sf = o; o = al16(o + gc);
   const size_t road_end = al16(L.hc + (size_t)cap_r * 11 * sizeof(float));
   L.road_end = road_end;
   if (o < road_end) o = road_end;
@@ -177,10 +176,12 @@ struct Sel {
   __device__ __forceinline__ float *ca() const { return reinterpret_cast<float *>(wb + L.ca); }
   __device__ __forceinline__ uint16_t *cp() const { return reinterpret_cast<uint16_t *>(wb + L.cp); }
   __device__ __forceinline__ float *ga() const { return reinterpret_cast<float *>(wb + L.ga); }
-  __device__ __forceinline__ double *ge() const { return reinterpret_cast<double *>(wb + L.ge); }
-  __device__ __forceinline__ int *gid() const { return reinterpret_cast<int *>(wb + L.gid); }
   __device__ __forceinline__ int *gpl() const { return reinterpret_cast<int *>(wb + L.gpl); }
-  __device__ __forceinline__ uint8_t *gf() const { return wb + L.gf; }
+  __device__ __forceinline__ float *sa() const { return reinterpret_cast<float *>(wb + L.sa); }
+  __device__ __forceinline__ int *spl() const { return reinterpret_cast<int *>(wb + L.spl); }
+  __device__ __forceinline__ int *sid() const { return reinterpret_cast<int *>(wb + L.sid); }
+  __device__ __forceinline__ double *se() const { return reinterpret_cast<double *>(wb + L.se); }
+  __device__ __forceinline__ uint8_t *sf() const { return wb + L.sf; }
   __device__ __forceinline__ int *sel_pl() const { return reinterpret_cast<int *>(wb + L.sel_pl); }
 };
 
@@ -373,22 +374,22 @@ __device__ int select_serial(const Src &src, int k, double radius, float r2hi, c
         bool take = true;
         if (cnt < k) {
           m = cnt++;
-        } else if (key_less(ej, idj, S.ge()[k - 1], S.gid()[k - 1])) {
+        } else if (key_less(ej, idj, S.se()[k - 1], S.sid()[k - 1])) {
           m = k - 1;
         } else {
           take = false;
           m = 0;
         }
         if (take) {
-          while (m > 0 && key_less(ej, idj, S.ge()[m - 1], S.gid()[m - 1])) {
-            S.ge()[m] = S.ge()[m - 1];
-            S.gid()[m] = S.gid()[m - 1];
-            S.gpl()[m] = S.gpl()[m - 1];
+          while (m > 0 && key_less(ej, idj, S.se()[m - 1], S.sid()[m - 1])) {
+            S.se()[m] = S.se()[m - 1];
+            S.sid()[m] = S.sid()[m - 1];
+            S.spl()[m] = S.spl()[m - 1];
             --m;
           }
-          S.ge()[m] = ej;
-          S.gid()[m] = idj;
-          S.gpl()[m] = plj;
+          S.se()[m] = ej;
+          S.sid()[m] = idj;
+          S.spl()[m] = plj;
         }
       }
       __syncwarp();
@@ -396,7 +397,7 @@ __device__ int select_serial(const Src &src, int k, double radius, float r2hi, c
   });
   cnt = __shfl_sync(kFull, cnt, 0);
   for (int m = lane; m < cnt; m += 32) {
-    S.sel_pl()[m] = S.gpl()[m];
+    S.sel_pl()[m] = S.spl()[m];
   }
   __syncwarp();
   return cnt;
@@ -419,99 +420,139 @@ __device__ __forceinline__ double hint_radius(float hint, double radius, double 
   return fmin((double)sqrtf(r2n), radius);
 }
 
-// Rank the set G[0, n_g) (bucket-sorted, counting-sort cursors in S.hc()) with
-// the float keys; near ties and possibly-out-of-radius keys get the exact
-// (distance, id) treatment.  Returns min(#valid, k); payloads in S.sel_pl().
-template <class Src>
-__device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float beta, float two_d,
-                        double r2, double D, double radius, int k, const Sel &S, int lane) {
-  // phase A: rank by float key; flag near ties and possibly-out-of-radius keys
+// Rank the set G[0, n_g) (bucket order, n_g <= 32 EPL).  Returns
+// min(#valid, k); payloads in S.sel_pl().
+//  sort    G is block-sorted (buckets are contiguous and ordered, strictly by
+//          key since bucket_of is monotone), so odd-even transposition rounds
+//          over the whole array (EPL consecutive positions per lane, +inf
+//          padding) sort it in cmax rounds, cmax = the largest bucket: a
+//          compare-exchange across a bucket boundary never swaps, so every
+//          bucket is sorted as its own segment;
+//  check   two sorted neighbours more than 2D apart are ordered exactly like
+//          their distances, so position t is the reference's rank unless t
+//          and a neighbour are a near tie, or its key may lie beyond the
+//          radius (a > r2 - D).  Every element before an unflagged t is
+//          exactly nearer and inside the radius.
+//  exact   (rare) flagged elements get the glibc-exact distance and id; a
+//          valid one ranks as the start of its near-tie cluster (a maximal
+//          run of neighbours <= 2D apart, all flagged) plus the valid
+//          cluster members that are exactly less.  Out-of-radius elements
+//          sort after every valid one, so they only reduce the count.
+__device__ __forceinline__ void cswap(float &ka, int &va, float &kb, int &vb) {
+  const bool sw = kb < ka;
+  const float k0 = sw ? kb : ka, k1 = sw ? ka : kb;
+  const int v0 = sw ? vb : va, v1 = sw ? va : vb;
+  ka = k0; kb = k1; va = v0; vb = v1;
+}
+
+template <int EPL, class Src>
+__device__ int rank_set(const Src &src, int n_g, int cmax, float two_d, double r2, double D,
+                        double radius, int k, const Sel &S, int lane) {
+  static_assert(EPL % 2 == 0, "odd-even rounds pair positions inside a lane");
   const float r2lo = __double2float_rd(r2 - D);
-  int flagged = 0;
-  // warp-uniform loops (the last pass predicates its idle lanes off, the
-  // window scan runs the warp's longest window for every lane): no
-  // divergent trip counts, so no reconvergence points inside
-  for (int p0 = 0; p0 < n_g; p0 += 32) {
-    const int p = p0 + lane;
-    const bool live = p < n_g;
-    const float ap = S.ga()[live ? p : n_g - 1];
-    const float t = ap * inv_w;
-    const int b = min((int)t, kNB - 1);   // = bucket_of(ap, inv_w), the scatter's bucket
-    const float fr = t - floorf(t);
-    const bool edge = fr < beta || fr > 1.0f - beta;
-    const int lo = edge ? (b > 0 ? b - 1 : 0) : b;
-    const int hi = edge ? (b < bmax ? b + 1 : bmax) : b;
-    const uint32_t hlo = S.hc()[lo], hhi = S.hc()[hi];
-    const int start = (int)(hlo >> 16) - (int)(hlo & 0xffffu);
-    const int len = live ? (int)(hhi >> 16) - start : 0;
-    const int wlen = (int)__reduce_max_sync(kFull, (unsigned)len);
-    const float dlo = ap - two_d, dhi = ap + two_d;
-    // window scan; p itself lies in the window (never below dlo, always
-    // inside the band: one band count is its own)
-    int rank = start, nband = 0;
-    for (int j = 0; j < wlen; ++j) {
-      const bool in = j < len;
-      const float aq = S.ga()[in ? start + j : p0];
-      rank += (in && aq < dlo) ? 1 : 0;
-      nband += (in && aq >= dlo && aq <= dhi) ? 1 : 0;
+  float key[EPL];
+  int val[EPL];
+  const int base = EPL * lane;
+  if constexpr (EPL % 4 == 0) {
+#pragma unroll
+    for (int e = 0; e < EPL; e += 4) {
+      const float4 kv = *reinterpret_cast<const float4 *>(S.ga() + base + e);
+      const int4 pv = *reinterpret_cast<const int4 *>(S.gpl() + base + e);
+      key[e] = kv.x; key[e + 1] = kv.y; key[e + 2] = kv.z; key[e + 3] = kv.w;
+      val[e] = pv.x; val[e + 1] = pv.y; val[e + 2] = pv.z; val[e + 3] = pv.w;
     }
-    const bool amb = nband > 1;
-    const uint8_t f = (amb ? 1 : 0) | (ap > r2lo ? 2 : 0) | (edge ? 8 : 0);
-    if (live) {
-      S.gf()[p] = f;
-      if (!(f & 3) && rank < k) S.sel_pl()[rank] = S.gpl()[p];
-      flagged += (f & 3) != 0;
+  } else {
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      key[e] = S.ga()[base + e];
+      val[e] = S.gpl()[base + e];
     }
   }
-  int n_invalid = 0;
-  if (__any_sync(kFull, flagged)) {
-    OBS_STAT(5, 1);
+#pragma unroll
+  for (int e = 0; e < EPL; ++e)
+    if (base + e >= n_g) key[e] = INFINITY;
+  for (int r = 0; r < cmax; ++r) {
+    if ((r & 1) == 0) {
+#pragma unroll
+      for (int e = 0; e < EPL; e += 2) cswap(key[e], val[e], key[e + 1], val[e + 1]);
+    } else {
+      // lane boundary pair (EPL l + EPL - 1, EPL (l + 1)): both sides read
+      // the other's value before either updates
+      const float kn = __shfl_down_sync(kFull, key[0], 1);
+      const int vn = __shfl_down_sync(kFull, val[0], 1);
+      const float kp = __shfl_up_sync(kFull, key[EPL - 1], 1);
+      const int vp = __shfl_up_sync(kFull, val[EPL - 1], 1);
+#pragma unroll
+      for (int e = 1; e + 1 < EPL; e += 2) cswap(key[e], val[e], key[e + 1], val[e + 1]);
+      if (lane < 31 && kn < key[EPL - 1]) { key[EPL - 1] = kn; val[EPL - 1] = vn; }
+      if (lane > 0 && kp > key[0]) { key[0] = kp; val[0] = vp; }
+    }
+  }
+  // check the first min(n_g, k) positions against their sorted neighbours
+  const int nk = n_g < k ? n_g : k;
+  const float kprev = __shfl_up_sync(kFull, key[EPL - 1], 1);
+  const float knext = __shfl_down_sync(kFull, key[0], 1);
+  bool flagged = false;
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    const float lo = e > 0 ? key[e - 1] : (lane > 0 ? kprev : -INFINITY);
+    const float hi = e + 1 < EPL ? key[e + 1] : (lane < 31 ? knext : INFINITY);
+    const bool amb = key[e] - lo <= two_d || hi - key[e] <= two_d;
+    if (base + e < nk) {
+      if (amb || key[e] > r2lo) flagged = true;
+      else S.sel_pl()[base + e] = val[e];
+    }
+  }
+  if (!__any_sync(kFull, flagged)) {
     __syncwarp();
-    // phase B: exact (distance, id) of the flagged elements
-    for (int p = lane; p < n_g; p += 32) {
-      const uint8_t f = S.gf()[p];
-      if (!(f & 3)) continue;
+    return nk;
+  }
+  OBS_STAT(5, 1);
+  float *const sa = S.sa();
+  int *const spl = S.spl();
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    if (base + e < n_g) {
+      sa[base + e] = key[e];
+      spl[base + e] = val[e];
+    }
+  }
+  __syncwarp();
+  // exact: flags over every position (clusters may run past k; the count of
+  // valid elements needs the top), exact (distance, id) of the flagged ones
+  int n_invalid = 0;
+  for (int t = lane; t < n_g; t += 32) {
+    const float at = sa[t];
+    const bool amb = (t > 0 && at - sa[t - 1] <= two_d) || (t + 1 < n_g && sa[t + 1] - at <= two_d);
+    uint8_t f = (amb ? 1 : 0) | (at > r2lo ? 2 : 0);
+    if (f) {
       int id;
-      const double e = src.exact(S.gpl()[p], id);
-      S.ge()[p] = e;
-      S.gid()[p] = id;
+      const double e = src.exact(spl[t], id);
+      S.se()[t] = e;
+      S.sid()[t] = id;
       if (e > radius) {
-        S.gf()[p] = f | 4;
+        f |= 4;
         ++n_invalid;
       }
     }
-    __syncwarp();
-    // phase C: rank the valid flagged elements (near ties compared exactly;
-    // ambiguity is symmetric, so both ends of a near tie carry exact keys)
-    for (int p = lane; p < n_g; p += 32) {
-      const uint8_t f = S.gf()[p];
-      if (!(f & 3) || (f & 4)) continue;
-      const float ap = S.ga()[p];
-      const int b = bucket_of(ap, inv_w);
-      const bool edge = f & 8;
-      const int lo = edge ? (b > 0 ? b - 1 : 0) : b;
-      const int hi = edge ? (b < bmax ? b + 1 : bmax) : b;
-      const uint32_t hlo = S.hc()[lo], hhi = S.hc()[hi];
-      const int start = (int)(hlo >> 16) - (int)(hlo & 0xffffu);
-      const int end = (int)(hhi >> 16);
-      const float dlo = ap - two_d, dhi = ap + two_d;
-      const double ep = S.ge()[p];
-      const int ip = S.gid()[p];
-      int rank = start;
-      for (int q = start; q < end; ++q) {
-        if (q == p) continue;
-        const float aq = S.ga()[q];
-        if (aq < dlo) {
-          ++rank;
-        } else if (aq <= dhi) {
-          if (!(S.gf()[q] & 4) && key_less(S.ge()[q], S.gid()[q], ep, ip)) ++rank;
-        }
-      }
-      if (rank < k) S.sel_pl()[rank] = S.gpl()[p];
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) n_invalid += __shfl_xor_sync(kFull, n_invalid, off);
+    S.sf()[t] = f;
   }
+  __syncwarp();
+  for (int t = lane; t < n_g; t += 32) {
+    const uint8_t f = S.sf()[t];
+    if (!f || (f & 4)) continue;
+    int c0 = t, c1 = t;
+    while (c0 > 0 && sa[c0] - sa[c0 - 1] <= two_d) --c0;
+    while (c1 + 1 < n_g && sa[c1 + 1] - sa[c1] <= two_d) ++c1;
+    const double et = S.se()[t];
+    const int it = S.sid()[t];
+    int rank = c0;
+    for (int q = c0; q <= c1; ++q)
+      if (q != t && !(S.sf()[q] & 4) && key_less(S.se()[q], S.sid()[q], et, it)) ++rank;
+    if (rank < k) S.sel_pl()[rank] = spl[t];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) n_invalid += __shfl_xor_sync(kFull, n_invalid, off);
   __syncwarp();
   const int n_valid = n_g - n_invalid;
   return n_valid < k ? n_valid : k;
@@ -532,7 +573,7 @@ __device__ int rank_set(const Src &src, int n_g, int bmax, float inv_w, float be
 // Exact ascending top-min(n_valid, k) by (distance, id).  Direct: small
 // candidate sets (partners) are compacted straight into G and ranked as one
 // bucket; a larger set takes the histogram path.
-template <bool Direct, class Src>
+template <bool Direct, int EPL, class Src>
 __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S, int lane,
                            double rho, float &bound_out) {
   if (k <= 0) return 0;
@@ -608,11 +649,9 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
       }
     }
     OBS_STAT(6, 1);
-    if (n <= S.gcap && n <= 0xffff) {
-      if (lane == 0) S.hc()[0] = ((uint32_t)n << 16) | (uint32_t)n;
-      __syncwarp();
-      // one bucket: inv_w = 0 puts every key on the bucket "edge" -> window 0..0
-      return rank_set(src, n, 0, 0.0f, beta, two_d, r2, D, radius, k, S, lane);
+    if (n <= S.gcap) {
+      // one block in visit order: n transposition rounds
+      return rank_set<EPL>(src, n, n, two_d, r2, D, radius, k, S, lane);
     }
     __syncwarp();
   }
@@ -704,6 +743,12 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     const uint32_t hb = S.hc()[bmax];   // (start << 16) | count of the last kept bucket
     n_g = (hb >> 16) + (hb & 0xffffu);
   }
+  // largest kept bucket: the sort's round count
+  int cmax = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q)
+    if (lane * kPer + q <= bmax) cmax = max(cmax, (int)cnt[q]);
+  cmax = (int)__reduce_max_sync(kFull, (unsigned)cmax);
   if (n_g > (uint32_t)S.gcap || total > 0xffffu) {
     OBS_STAT(3, 1);
     src.restrict_to(radius + 1e-6, lane);
@@ -736,7 +781,7 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     });
   }
   __syncwarp();
-  return rank_set(src, (int)n_g, bmax, inv_w, beta, two_d, r2, D, radius, k, S, lane);
+  return rank_set<EPL>(src, (int)n_g, cmax, two_d, r2, D, radius, k, S, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -768,6 +813,9 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t pts_bar;
   constexpr bool kFixed = CAPA > 0;
+  // G positions per lane in the sort (even; runtime caps <= kSelCap: 6)
+  constexpr int kEPL = kFixed ? ((gcap_of(CAPA, CAPR) + 63) / 64) * 2 : 2 * ((kSelCap + 48 + 63) / 64);
+  static_assert(32 * kEPL >= (kFixed ? gcap_of(CAPA, CAPR) : kSelCap + 48), "sort capacity");
   const int cap_a = kFixed ? CAPA : C.max_agents_obs, cap_r = kFixed ? CAPR : C.max_road_points_obs;
   constexpr WarpLayout kWL = make_layout(CAPA, CAPR, !SharedPts);
   const WarpLayout WL = kFixed ? kWL : warp_layout(C, !SharedPts);
@@ -886,7 +934,7 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     // while the selected road records are in flight
     PartnerSrc psrc{ax, ay, AT.vis, A, i, px, py};
     float no_bound = 0.0f;
-    const int ma = select_topk<true>(psrc, cap_a, radius, D_fp64, S, lane, radius, no_bound);
+    const int ma = select_topk<true, kEPL>(psrc, cap_a, radius, D_fp64, S, lane, radius, no_bound);
     int *const psel = reinterpret_cast<int *>(wb + WL.psel);
     for (int m = lane; m < ma; m += 32) psel[m] = S.sel_pl()[m];
     __syncwarp();
@@ -916,13 +964,13 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
         RoadSrcShared rsrc{pts, static_cast<const ds_point_rec *>(T.gpt_rec), (int)p0, prx, pry, px,
                            py, &geo, reinterpret_cast<int *>(wb + WL.fr)};
         rsrc.cover(rho < radius ? rho : reach, lane);
-        mr = select_topk<false>(rsrc, cap_r, radius, D, S, lane, rho, bound);
+        mr = select_topk<false, kEPL>(rsrc, cap_r, radius, D, S, lane, rho, bound);
       } else {
         const double rho = hint_radius(rho_hint, radius, D_fp64);
         RoadSrcGlobal rsrc{T.gpt_x, T.gpt_y, T.gpt_id, (int)p0, np, px, py, &geo,
                            reinterpret_cast<int *>(wb + WL.fr)};
         rsrc.cover(rho < radius ? rho : reach, lane);
-        mr = select_topk<false>(rsrc, cap_r, radius, D_fp64, S, lane, rho, bound);
+        mr = select_topk<false, kEPL>(rsrc, cap_r, radius, D_fp64, S, lane, rho, bound);
       }
     }
     if (St.obs_hint && lane == 0)
