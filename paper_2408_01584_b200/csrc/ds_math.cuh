@@ -23,26 +23,26 @@ constexpr double kTwoPi = 6.283185307179586;   // 2.0 * math.pi (exact doubling)
 // Angle wrap of _fastpath._wrap (fp:206-212) / geometry.wrap_angle_arr
 // (geo:70-72): r = (theta + pi) mod 2pi - pi with Python's floor-mod sign
 // rule, then +2pi if r <= -pi.  fmod is exact, so this is bit-reproducible.
+// floor-mod of a by 2pi outside [-2pi, 4pi) (fmod, then the sign rule)
+DS_HD double wrap_far(double a) {
+  double r = fmod(a, kTwoPi);
+  if (r != 0.0) {
+    if (r < 0.0) r += kTwoPi;
+  } else {
+    r = 0.0;  // copysign(0, 2pi)
+  }
+  return r;
+}
+
+// Branch-free on [-2pi, 4pi): fmod(a, 2pi) is a, a - 2pi (exact, Sterbenz)
+// or a (a < 0, then the sign rule adds 2pi: one rounding, a + 2pi).
 DS_HD double wrap(double theta) {
   const double a = theta + kPi;
-  double r;
-  if (a >= 0.0 && a < kTwoPi) {
-    r = a;                      // fmod(a, 2pi) == a
-  } else if (a >= kTwoPi && a < 2.0 * kTwoPi) {
-    r = a - kTwoPi;             // exact (Sterbenz), == fmod(a, 2pi)
-  } else if (a < 0.0 && a >= -kTwoPi) {
-    r = a + kTwoPi;             // fmod(a, 2pi) == a < 0, then += 2pi
-  } else {
-    r = fmod(a, kTwoPi);
-    if (r != 0.0) {
-      if (r < 0.0) r += kTwoPi;
-    } else {
-      r = 0.0;  // copysign(0, 2pi)
-    }
-  }
+  double r = a >= kTwoPi ? a - kTwoPi : a;
+  r = a < 0.0 ? a + kTwoPi : r;
+  if (!(a >= -kTwoPi && a < 2.0 * kTwoPi)) r = wrap_far(a);
   r = r - kPi;
-  if (r <= -kPi) r += kTwoPi;
-  return r;
+  return r <= -kPi ? r + kTwoPi : r;
 }
 
 // np.mod(a, 2 pi) (numpy's npy_divmod: fmod, then +2pi for a negative

@@ -445,6 +445,69 @@ __device__ __forceinline__ void cswap(float &ka, int &va, float &kb, int &vb) {
   ka = k0; kb = k1; va = v0; vb = v1;
 }
 
+// The exact tail of rank_set (rare: a near tie or a possibly-out-of-radius
+// key among the first k): G sorted in S.sa() / S.spl().
+template <class Src>
+__device__ int rank_exact(const Src &src, int n_g, float two_d, float r2lo,
+                                       double radius, int k, const Sel &S, int lane) {
+  const float *const sa = S.sa();
+  const int *const spl = S.spl();
+  // exact: flags over every position (clusters may run past k; the count of
+  // valid elements needs the top), exact (distance, id) of the flagged ones
+  int n_invalid = 0;
+  for (int t = lane; t < n_g; t += 32) {
+    const float at = sa[t];
+    const bool amb = (t > 0 && at - sa[t - 1] <= two_d) || (t + 1 < n_g && sa[t + 1] - at <= two_d);
+    uint8_t f = (amb ? 1 : 0) | (at > r2lo ? 2 : 0);
+    if (f) {
+      int id;
+      const double e = src.exact(spl[t], id);
+      S.se()[t] = e;
+      S.sid()[t] = id;
+      if (e > radius) {
+        f |= 4;
+        ++n_invalid;
+      }
+    }
+    S.sf()[t] = f;
+  }
+  __syncwarp();
+  for (int t = lane; t < n_g; t += 32) {
+    const uint8_t f = S.sf()[t];
+    if (!f || (f & 4)) continue;
+    int c0 = t, c1 = t;
+    while (c0 > 0 && sa[c0] - sa[c0 - 1] <= two_d) --c0;
+    while (c1 + 1 < n_g && sa[c1 + 1] - sa[c1] <= two_d) ++c1;
+    const double et = S.se()[t];
+    const int it = S.sid()[t];
+    int rank = c0;
+    for (int q = c0; q <= c1; ++q)
+      if (q != t && !(S.sf()[q] & 4) && key_less(S.se()[q], S.sid()[q], et, it)) ++rank;
+    if (rank < k) S.sel_pl()[rank] = spl[t];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) n_invalid += __shfl_xor_sync(kFull, n_invalid, off);
+  __syncwarp();
+  const int n_valid = n_g - n_invalid;
+  return n_valid < k ? n_valid : k;
+}
+
+// Exact ascending top-min(n_valid, k) by (distance, id) given candidate keys
+// with |a - d^2| <= D.  Payloads land in S.sel_pl()[0..m).  Warp-collective.
+//  * rho: the radius the source currently covers (< radius when the caller
+//    narrowed it with a search hint, see hint_radius).  A narrowed pass 1 is
+//    used only if every bucket the selection touches provably lies inside
+//    the disc ((bmax + 1) w + D <= rho^2), else it reruns on the full radius.
+//    On return, bound_out holds a bound on the k-th distance (0 when fewer
+//    than k candidates exist).
+//  * ranking uses the float keys: two keys more than 2D apart are ordered
+//    exactly as the distances, so the exact FP64 hypot is evaluated only for
+//    near ties (|a_p - a_q| <= 2D) and possible out-of-radius keys.
+// Buffered: pass 1 keeps (key, payload) in shared memory (global-points path).
+// Exact ascending top-min(n_valid, k) by (distance, id).  Direct: small
+// candidate sets (partners) are compacted straight into G and ranked as one
+// bucket; a larger set takes the histogram path.
+
 template <int EPL, class Src>
 __device__ int rank_set(const Src &src, int n_g, int cmax, float two_d, double r2, double D,
                         double radius, int k, const Sel &S, int lane) {
@@ -508,71 +571,17 @@ __device__ int rank_set(const Src &src, int n_g, int cmax, float two_d, double r
     return nk;
   }
   OBS_STAT(5, 1);
-  float *const sa = S.sa();
-  int *const spl = S.spl();
 #pragma unroll
   for (int e = 0; e < EPL; ++e) {
     if (base + e < n_g) {
-      sa[base + e] = key[e];
-      spl[base + e] = val[e];
+      S.sa()[base + e] = key[e];
+      S.spl()[base + e] = val[e];
     }
   }
   __syncwarp();
-  // exact: flags over every position (clusters may run past k; the count of
-  // valid elements needs the top), exact (distance, id) of the flagged ones
-  int n_invalid = 0;
-  for (int t = lane; t < n_g; t += 32) {
-    const float at = sa[t];
-    const bool amb = (t > 0 && at - sa[t - 1] <= two_d) || (t + 1 < n_g && sa[t + 1] - at <= two_d);
-    uint8_t f = (amb ? 1 : 0) | (at > r2lo ? 2 : 0);
-    if (f) {
-      int id;
-      const double e = src.exact(spl[t], id);
-      S.se()[t] = e;
-      S.sid()[t] = id;
-      if (e > radius) {
-        f |= 4;
-        ++n_invalid;
-      }
-    }
-    S.sf()[t] = f;
-  }
-  __syncwarp();
-  for (int t = lane; t < n_g; t += 32) {
-    const uint8_t f = S.sf()[t];
-    if (!f || (f & 4)) continue;
-    int c0 = t, c1 = t;
-    while (c0 > 0 && sa[c0] - sa[c0 - 1] <= two_d) --c0;
-    while (c1 + 1 < n_g && sa[c1 + 1] - sa[c1] <= two_d) ++c1;
-    const double et = S.se()[t];
-    const int it = S.sid()[t];
-    int rank = c0;
-    for (int q = c0; q <= c1; ++q)
-      if (q != t && !(S.sf()[q] & 4) && key_less(S.se()[q], S.sid()[q], et, it)) ++rank;
-    if (rank < k) S.sel_pl()[rank] = spl[t];
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) n_invalid += __shfl_xor_sync(kFull, n_invalid, off);
-  __syncwarp();
-  const int n_valid = n_g - n_invalid;
-  return n_valid < k ? n_valid : k;
+  return rank_exact(src, n_g, two_d, r2lo, radius, k, S, lane);
 }
 
-// Exact ascending top-min(n_valid, k) by (distance, id) given candidate keys
-// with |a - d^2| <= D.  Payloads land in S.sel_pl()[0..m).  Warp-collective.
-//  * rho: the radius the source currently covers (< radius when the caller
-//    narrowed it with a search hint, see hint_radius).  A narrowed pass 1 is
-//    used only if every bucket the selection touches provably lies inside
-//    the disc ((bmax + 1) w + D <= rho^2), else it reruns on the full radius.
-//    On return, bound_out holds a bound on the k-th distance (0 when fewer
-//    than k candidates exist).
-//  * ranking uses the float keys: two keys more than 2D apart are ordered
-//    exactly as the distances, so the exact FP64 hypot is evaluated only for
-//    near ties (|a_p - a_q| <= 2D) and possible out-of-radius keys.
-// Buffered: pass 1 keeps (key, payload) in shared memory (global-points path).
-// Exact ascending top-min(n_valid, k) by (distance, id).  Direct: small
-// candidate sets (partners) are compacted straight into G and ranked as one
-// bucket; a larger set takes the histogram path.
 template <bool Direct, int EPL, class Src>
 __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S, int lane,
                            double rho, float &bound_out) {
@@ -591,7 +600,9 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     // any scale works here (histogram, scatter and ranking all bucket by
     // a * inv_w; the edge bands are in those units and the window check
     // keeps a 1 % slack on w): the fast division, no IEEE slow path
-    inv_w = r2hi > 0.0f ? __fdividef((float)kNB, r2hi) : 0.0f;
+    float rcp;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(r2hi));
+    inv_w = r2hi > 0.0f ? (float)kNB * rcp : 0.0f;
     w = (double)r2hi / kNB;
     // edge band in bucket units: twice the key error plus float slack
     beta = 2.0f * Df * inv_w + 4e-5f;

@@ -40,33 +40,42 @@ __device__ __forceinline__ void write_row(const ObsOut &o, int64_t orow, const f
   if (o.dtype == DS_OBS_F32) {
     float *out = static_cast<float *>(o.base) + orow * (int64_t)o.stride;
     const int ph = (int)((reinterpret_cast<uintptr_t>(out) >> 2) & 3);
-    const bool vec = ((reinterpret_cast<uintptr_t>(row) >> 2) & 3) == (uintptr_t)ph;
-    const int head = vec ? ((4 - ph) & 3) : width;
-    const int nvec = vec && width > head ? (width - head) >> 2 : 0;
-    const int tail0 = head < width ? head + 4 * nvec : width;
-    if (lane < head && lane < width) out[lane] = scaled(row, scale, lane);
-    const float4 *rv = reinterpret_cast<const float4 *>(row + head) + lane;
-    float4 *ov = reinterpret_cast<float4 *>(out + head) + lane;
-    const int nv = nvec > lane ? (nvec - lane + 31) >> 5 : 0;   // this lane's vectors
-    if (!scale) {
-#pragma unroll 4
-      for (int q = 0; q < nv; ++q) ov[32 * q] = rv[32 * q];
-    } else {
+    if (((reinterpret_cast<uintptr_t>(row) >> 2) & 3) != (uintptr_t)ph) {
+      // phases differ (callers stage rows phase-matched): scalar copy
 #pragma unroll 1
-      for (int q = 0; q < nv; ++q) {
-        float4 x = rv[32 * q];
-        const float *sc = scale + head + 4 * (lane + 32 * q);
-        x.x = __fdiv_rn(x.x, sc[0]);
-        x.y = __fdiv_rn(x.y, sc[1]);
-        x.z = __fdiv_rn(x.z, sc[2]);
-        x.w = __fdiv_rn(x.w, sc[3]);
-        ov[32 * q] = x;
+      for (int c = lane; c < width; c += 32) out[c] = scaled(row, scale, c);
+    } else {
+      // <= 3 head floats up to the 16-B boundary, float4 body, <= 3 tail
+      // floats: head and tail are one predicated store each (lanes 0-3 /
+      // 4-7), the body one 16-B store per lane and pass
+      const int head = min((4 - ph) & 3, width);
+      const int nvec = (width - head) >> 2;
+      const int tail0 = head + 4 * nvec;
+      const int c = lane < 4 ? lane : tail0 + lane - 4;
+      if (lane < 4 ? lane < head : (lane < 8 && c < width)) out[c] = scaled(row, scale, c);
+      const float4 *rv = reinterpret_cast<const float4 *>(row + head) + lane;
+      float4 *ov = reinterpret_cast<float4 *>(out + head) + lane;
+      const int nv = nvec > lane ? (nvec - lane + 31) >> 5 : 0;   // this lane's vectors
+      if (!scale) {
+#pragma unroll 4
+        for (int q = 0; q < nv; ++q) ov[32 * q] = rv[32 * q];
+      } else {
+#pragma unroll 1
+        for (int q = 0; q < nv; ++q) {
+          float4 x = rv[32 * q];
+          const float *sc = scale + head + 4 * (lane + 32 * q);
+          x.x = __fdiv_rn(x.x, sc[0]);
+          x.y = __fdiv_rn(x.y, sc[1]);
+          x.z = __fdiv_rn(x.z, sc[2]);
+          x.w = __fdiv_rn(x.w, sc[3]);
+          ov[32 * q] = x;
+        }
       }
     }
+    if (o.stride > width) {
 #pragma unroll 1
-    for (int c = tail0 + lane; c < width; c += 32) out[c] = scaled(row, scale, c);
-#pragma unroll 1
-    for (int c = width + lane; c < o.stride; c += 32) out[c] = 0.0f;
+      for (int c = width + lane; c < o.stride; c += 32) out[c] = 0.0f;
+    }
     return;
   }
   __nv_bfloat16 *out = static_cast<__nv_bfloat16 *>(o.base) + orow * (int64_t)o.stride;
