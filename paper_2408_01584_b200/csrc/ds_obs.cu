@@ -121,29 +121,48 @@ __host__ __device__ inline WarpLayout warp_layout(const ds_config &c, bool buffe
 }
 
 // Per-agent tables staged once per world (structure of arrays):
-//   x, y, heading, speed, length, width, cos, sin (f64) | search hint (float4)
-//   | ego block (7 floats, padded to 8) | flags (u16) | visible (u8)
-//   | row -> local agent (u16)
+//   x, y, heading, speed, cos, sin (f64) | length, width (f32: only their
+//   float32 values are observed) | ego block (7
+//   floats, padded to 8) | road-selection parameters (RoadPre) | flags (u16)
+//   | visible (u8) | row -> local agent (u16)
+// RoadPre: everything the road selection of one agent needs that does not
+// depend on the candidates, formed by one thread per agent in the prologue
+// (instead of by every lane of the agent's warp):
+//   a = (prx, pry, marg, Df): grid-relative float position, the RowGeo float
+//       margin, Df >= D
+//   b = (r2hi, inv_w, two_d, r2lo): the first histogram range
+//   c = (D, rho): the key error bound and the covered radius
+//   d = (iy0, nrows, flags): the disc's cell rows; flags 1 = restricted
+//       (hint-narrowed), 2 = serial
 struct AgentTabs {
-  double *x, *y, *h, *v, *l, *w, *c, *s;
-  float4 *hint;
+  double *x, *y, *h, *v, *c, *s;
+  float *l, *w;
   float *ego;
+  float4 *pa, *pb;
+  double2 *pc;
+  int4 *pd;
   uint16_t *flg, *rloc;
   uint8_t *vis;
 };
 
 __host__ __device__ inline size_t agents_bytes(int amax) {
-  return (size_t)amax * (8 * sizeof(double) + sizeof(float4) + 8 * sizeof(float)) +
+  return (size_t)amax * (6 * sizeof(double) + 2 * sizeof(float) + 8 * sizeof(float) +
+                         3 * sizeof(float4) + sizeof(double2)) +
          al16((size_t)amax * sizeof(uint16_t)) * 2 + al16((size_t)amax);
 }
 
 __device__ inline AgentTabs agent_tabs(unsigned char *base, int amax) {
   AgentTabs t;
-  double *d = reinterpret_cast<double *>(base);
-  t.x = d; t.y = d + amax; t.h = d + 2 * amax; t.v = d + 3 * amax;
-  t.l = d + 4 * amax; t.w = d + 5 * amax; t.c = d + 6 * amax; t.s = d + 7 * amax;
-  unsigned char *o = base + (size_t)amax * 8 * sizeof(double);
-  t.hint = reinterpret_cast<float4 *>(o); o += (size_t)amax * sizeof(float4);
+  unsigned char *o = base;
+  t.pa = reinterpret_cast<float4 *>(o); o += (size_t)amax * sizeof(float4);
+  t.pb = reinterpret_cast<float4 *>(o); o += (size_t)amax * sizeof(float4);
+  t.pc = reinterpret_cast<double2 *>(o); o += (size_t)amax * sizeof(double2);
+  t.pd = reinterpret_cast<int4 *>(o); o += (size_t)amax * sizeof(int4);
+  double *d = reinterpret_cast<double *>(o);
+  t.x = d; t.y = d + amax; t.h = d + 2 * amax; t.v = d + 3 * amax; t.c = d + 4 * amax; t.s = d + 5 * amax;
+  o += (size_t)amax * 6 * sizeof(double);
+  t.l = reinterpret_cast<float *>(o); o += (size_t)amax * sizeof(float);
+  t.w = reinterpret_cast<float *>(o); o += (size_t)amax * sizeof(float);
   t.ego = reinterpret_cast<float *>(o); o += (size_t)amax * 8 * sizeof(float);
   t.flg = reinterpret_cast<uint16_t *>(o); o += al16((size_t)amax * sizeof(uint16_t));
   t.rloc = reinterpret_cast<uint16_t *>(o); o += al16((size_t)amax * sizeof(uint16_t));
@@ -492,27 +511,10 @@ __device__ int rank_exact(const Src &src, int n_g, float two_d, float r2lo,
   return n_valid < k ? n_valid : k;
 }
 
-// Exact ascending top-min(n_valid, k) by (distance, id) given candidate keys
-// with |a - d^2| <= D.  Payloads land in S.sel_pl()[0..m).  Warp-collective.
-//  * rho: the radius the source currently covers (< radius when the caller
-//    narrowed it with a search hint, see hint_radius).  A narrowed pass 1 is
-//    used only if every bucket the selection touches provably lies inside
-//    the disc ((bmax + 1) w + D <= rho^2), else it reruns on the full radius.
-//    On return, bound_out holds a bound on the k-th distance (0 when fewer
-//    than k candidates exist).
-//  * ranking uses the float keys: two keys more than 2D apart are ordered
-//    exactly as the distances, so the exact FP64 hypot is evaluated only for
-//    near ties (|a_p - a_q| <= 2D) and possible out-of-radius keys.
-// Buffered: pass 1 keeps (key, payload) in shared memory (global-points path).
-// Exact ascending top-min(n_valid, k) by (distance, id).  Direct: small
-// candidate sets (partners) are compacted straight into G and ranked as one
-// bucket; a larger set takes the histogram path.
-
 template <int EPL, class Src>
-__device__ int rank_set(const Src &src, int n_g, int cmax, float two_d, double r2, double D,
-                        double radius, int k, const Sel &S, int lane) {
+__device__ int rank_set(const Src &src, int n_g, int cmax, float two_d, float r2lo, double radius,
+                        int k, const Sel &S, int lane) {
   static_assert(EPL % 2 == 0, "odd-even rounds pair positions inside a lane");
-  const float r2lo = __double2float_rd(r2 - D);
   float key[EPL];
   int val[EPL];
   const int base = EPL * lane;
@@ -582,36 +584,75 @@ __device__ int rank_set(const Src &src, int n_g, int cmax, float two_d, double r
   return rank_exact(src, n_g, two_d, r2lo, radius, k, S, lane);
 }
 
-template <bool Direct, int EPL, class Src>
-__device__ int select_topk(Src src, int k, double radius, double D, const Sel &S, int lane,
-                           double rho, float &bound_out) {
-  if (k <= 0) return 0;
-  const double r2 = radius * radius;
-  // float thresholds rounded the conservative way: Df >= D (wider bands),
-  // r2lo <= r2 - D (more keys get the exact radius test)
-  const float Df = __double2float_ru(D);
-  const float r2lo = __double2float_rd(r2 - D);
-  // histogram range [0, r2hi] in key units: the whole disc, or [0, rho^2]
-  // for a hint-narrowed scan (finer buckets, see hint_radius)
+// Histogram range [0, r2hi] in key units (the whole disc r^2 + D, or rho^2
+// for a hint-narrowed scan): the bucket scale inv_w (any scale works here --
+// histogram, scatter and ranking all bucket by a * inv_w; the edge bands are
+// in those units and the window check keeps a 1 % slack on w, so the fast
+// reciprocal), the edge band beta in bucket units (twice the key error plus
+// float slack) and the near-tie band two_d (padded by the float rounding of
+// a - 2D).
+struct SelRange {
   float r2hi, inv_w, beta, two_d;
-  double w;
-  auto set_range = [&](double top) {
-    r2hi = (float)(top * (1.0 + 1e-7) + 1e-30);
-    // any scale works here (histogram, scatter and ranking all bucket by
-    // a * inv_w; the edge bands are in those units and the window check
-    // keeps a 1 % slack on w): the fast division, no IEEE slow path
-    float rcp;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(r2hi));
-    inv_w = r2hi > 0.0f ? (float)kNB * rcp : 0.0f;
-    w = (double)r2hi / kNB;
-    // edge band in bucket units: twice the key error plus float slack
-    beta = 2.0f * Df * inv_w + 4e-5f;
-    // near-tie band in float, padded by the float rounding of a - 2D
-    two_d = 2.0f * Df + 2.5e-7f * r2hi;
+};
+
+__host__ __device__ __forceinline__ SelRange range_of(double top, float Df) {
+  SelRange R;
+  R.r2hi = (float)(top * (1.0 + 1e-7) + 1e-30);
+#ifdef __CUDA_ARCH__
+  float rcp;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(R.r2hi));
+#else
+  const float rcp = 1.0f / R.r2hi;
+#endif
+  R.inv_w = R.r2hi > 0.0f ? (float)kNB * rcp : 0.0f;
+  R.beta = 2.0f * Df * R.inv_w + 4e-5f;
+  R.two_d = 2.0f * Df + 2.5e-7f * R.r2hi;
+  return R;
+}
+
+// Per-selection parameters (formed once per agent in the prologue for the
+// road points, once per launch on the host for the partners).
+//  Df >= D and r2lo <= r2 - D: float thresholds rounded the conservative way
+//  (wider bands, more keys get the exact radius test); R: the first range
+//  (narrowed to rho when `restricted`); serial: the full-radius key bound is
+//  too loose for the bucket width (beta >= 1/8): serial insertion.
+struct SelParams {
+  SelRange R;
+  float Df, r2lo;
+  double D, rho;
+  bool restricted, serial;
+};
+
+// Exact ascending top-min(n_valid, k) by (distance, id) given candidate keys
+// with |a - d^2| <= D.  Payloads land in S.sel_pl()[0..m).  Warp-collective.
+//  * Direct: small candidate sets (partners) are compacted straight into G
+//    and ranked by counting; a larger set takes the histogram path.
+//  * rho: the radius the source currently covers (< radius when the caller
+//    narrowed it with a search hint, see hint_radius).  A narrowed pass 1 is
+//    used only if every bucket the selection touches provably lies inside
+//    the disc ((bmax + 1) w + D <= rho^2), else it reruns on the full radius.
+//    On return, bound_out holds a bound on the k-th distance (0 when fewer
+//    than k candidates exist).
+//  * ranking uses the float keys: two keys more than 2D apart are ordered
+//    exactly as the distances, so the exact FP64 hypot is evaluated only for
+//    near ties (|a_p - a_q| <= 2D) and possible out-of-radius keys.
+//  * pass 1 keeps (key, payload) in shared memory when they fit.
+template <bool Direct, int EPL, class Src>
+__device__ int select_topk(Src src, int k, double radius, const SelParams &P, const Sel &S,
+                           int lane, float &bound_out) {
+  if (k <= 0) return 0;
+  const double r2 = radius * radius, D = P.D, rho = P.rho;
+  const float Df = P.Df, r2lo = P.r2lo;
+  float r2hi = P.R.r2hi, inv_w = P.R.inv_w, two_d = P.R.two_d;
+  auto set_full = [&]() {
+    const SelRange F = range_of(r2 + D, Df);
+    r2hi = F.r2hi;
+    inv_w = F.inv_w;
+    two_d = F.two_d;
   };
-  set_range(r2 + D);
-  if (!(beta < 0.125f)) {
+  if (P.serial) {
     OBS_STAT(3, 1);
+    set_full();
     return select_serial(src, k, radius, r2hi, S, lane);
   }
   if (Direct) {
@@ -634,18 +675,17 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
       // distances, so the ranks are the reference's unless a near tie or a
       // possibly-out-of-radius key sits inside the first k (then the exact
       // ranking below decides)
-      // (non-negative float keys order like their bit patterns: one 64-bit
-      // compare of (key bits, payload) per broadcast; near ties are found
-      // afterwards between sorted neighbours, staged in the idle pass-1 buffer)
       const float a = lane < n ? S.ga()[lane] : INFINITY;
       const int pl = lane < n ? S.gpl()[lane] : 0x7fffffff;
       // (key, payload) order = (key bits, lane): G was compacted in visit
       // order, so payloads ascend with the lane.  One 32-bit shuffle per
-      // broadcast key; equal keys are ranked by lane with one match.
+      // broadcast key (non-negative floats order like their bit patterns);
+      // equal keys are ranked by lane with one match.
       const unsigned ab = __float_as_uint(a);
       int rank = __popc(__match_any_sync(kFull, ab) & ((1u << lane) - 1u));
 #pragma unroll 4
       for (int j = 0; j < n; ++j) rank += __shfl_sync(kFull, ab, j) < ab ? 1 : 0;
+      // near ties between sorted neighbours, staged in the idle pass-1 buffer
       float *const srt = S.ca();
       if (lane < n) srt[rank] = a;
       __syncwarp();
@@ -662,18 +702,18 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     OBS_STAT(6, 1);
     if (n <= S.gcap) {
       // one block in visit order: n transposition rounds
-      return rank_set<EPL>(src, n, n, two_d, r2, D, radius, k, S, lane);
+      return rank_set<EPL>(src, n, n, two_d, r2lo, radius, k, S, lane);
     }
     __syncwarp();
   }
-  bool restricted = rho < radius;
-  if (restricted) set_range(rho * rho);
+  bool restricted = P.restricted;
   const int pb = src.pbase();
   const bool small = src.small_payload();
   constexpr int kPer = kNB / 32;
   uint32_t total, n_g, incl, local;
   uint32_t cnt[kPer];
   int bstar, bmax, nbuf;
+  double w;   // bucket width (key units)
   static_assert(kPer % 4 == 0, "the histogram is read / written as uint4 per lane");
   constexpr int kVec = kPer / 4;
   uint4 *const hc4 = reinterpret_cast<uint4 *>(S.hc());
@@ -725,13 +765,14 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     // inversion with b* at their shared edge, and its window never needs
     // b*+2 (all of b*+2 lies above it); edge windows are clamped to bmax
     bmax = min(bstar + 1, kNB - 1);
+    w = (double)r2hi / kNB;
     // a narrowed scan is valid only if all buckets <= bmax lie inside the disc
     OBS_STAT(1, total);
     if (restricted && !((((double)bmax + 1.01) * w + D) <= rho * rho)) {
       OBS_STAT(2, 1);
       src.restrict_to(radius + 1e-6, lane);
       restricted = false;
-      set_range(r2 + D);
+      set_full();
       continue;
     }
     break;
@@ -792,7 +833,7 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
     });
   }
   __syncwarp();
-  return rank_set<EPL>(src, (int)n_g, cmax, two_d, r2, D, radius, k, S, lane);
+  return rank_set<EPL>(src, (int)n_g, cmax, two_d, r2lo, radius, k, S, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -805,6 +846,9 @@ __device__ int select_topk(Src src, int k, double radius, double D, const Sel &S
 // keeping (or rematerialising) them in registers.
 struct RadialK {
   double radius, reach, r2, D_fp64, cs, inv_cs, key_e;
+  // the partners' selection parameters (SelParams of the full disc)
+  float p_r2hi, p_inv_w, p_two_d, p_Df, p_r2lo;
+  bool p_serial;
 };
 
 template <int WARPS, bool SharedPts, int CAPA, int CAPR>
@@ -878,33 +922,6 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   float *const row0 = reinterpret_cast<float *>(wb + WL.row);
   const int row0_phase = (int)((reinterpret_cast<uintptr_t>(row0) >> 2) & 3);
 
-  // agent tables, the ego block of every agent (fp:228-238) and the search
-  // hints: one thread per agent, overlapping the points' bulk copy
-  for (int i = threadIdx.x; i < A; i += blockDim.x) {
-    const int64_t g = a0 + i;
-    const double px = St.x[g], py = St.y[g], hd = St.heading[g], v = St.speed[g];
-    const double ln = T.length[g], wd = T.width[g];
-    const double gx = T.goal_x[g] - px, gy = T.goal_y[g] - py;
-    const uint16_t f = St.flags[g];
-    AT.hint[i] = St.obs_hint ? reinterpret_cast<const float4 *>(St.obs_hint)[g]
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-    double sh, ch;
-    sincos(hd, &sh, &ch);
-    AT.x[i] = px; AT.y[i] = py; AT.h[i] = hd; AT.v[i] = v;
-    AT.l[i] = ln; AT.w[i] = wd; AT.c[i] = ch; AT.s[i] = sh;
-    AT.flg[i] = f;
-    AT.vis[i] = (f & DS_F_PRESENT) && !(f & DS_F_REMOVED);
-    float *e = AT.ego + 8 * i;
-    e[0] = (float)v;
-    e[1] = (float)ln;
-    e[2] = (float)wd;
-    e[3] = (float)(gx * ch + gy * sh);
-    e[4] = (float)(gy * ch - gx * sh);
-    e[5] = (float)hypot(gx, gy);
-    e[6] = (f & DS_F_COLLIDED) ? 1.0f : 0.0f;
-  }
-  // row -> local agent, so the row loop starts from shared memory
-  for (int r = threadIdx.x; r < nrow; r += blockDim.x) AT.rloc[r] = (uint16_t)(T.row_agent[c0 + r] - a0);
   const double radius = K.radius;
   const double reach = K.reach;         // culling slack; membership is decided exactly
   const int road_off = 7 + 7 * cap_a;
@@ -915,10 +932,75 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   const int64_t cbase = T.grid_cell_off[w];
   const double eps_p = SharedPts ? T.grid_eps[w] : 0.0;
   const double D_fp64 = K.D_fp64;       // fl32 of an FP64 d^2
+
+  // agent tables, the ego block of every agent (fp:228-238), the search
+  // hints and the road-selection parameters: one thread per agent,
+  // overlapping the points' bulk copy
+  for (int i = threadIdx.x; i < A; i += blockDim.x) {
+    const int64_t g = a0 + i;
+    const double px = St.x[g], py = St.y[g], hd = St.heading[g], v = St.speed[g];
+    const double ln = T.length[g], wd = T.width[g];
+    const double gx = T.goal_x[g] - px, gy = T.goal_y[g] - py;
+    const uint16_t f = St.flags[g];
+    const float4 hint = St.obs_hint ? reinterpret_cast<const float4 *>(St.obs_hint)[g]
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    double sh, ch;
+    sincos(hd, &sh, &ch);
+    AT.x[i] = px; AT.y[i] = py; AT.h[i] = hd; AT.v[i] = v;
+    AT.l[i] = (float)ln; AT.w[i] = (float)wd; AT.c[i] = ch; AT.s[i] = sh;
+    AT.flg[i] = f;
+    AT.vis[i] = (f & DS_F_PRESENT) && !(f & DS_F_REMOVED);
+    float *e = AT.ego + 8 * i;
+    e[0] = (float)v;
+    e[1] = (float)ln;
+    e[2] = (float)wd;
+    e[3] = (float)(gx * ch + gy * sh);
+    e[4] = (float)(gy * ch - gx * sh);
+    e[5] = (float)hypot(gx, gy);
+    e[6] = (f & DS_F_COLLIDED) ? 1.0f : 0.0f;
+    // road selection: the bound on this step's k-th distance is the hint
+    // plus the distance moved (float; the 1 mm slack exceeds the rounding of
+    // the grid-relative floats)
+    const double rx = px - gx0, ry = py - gy0;
+    const float prx = (float)rx, pry = (float)ry;
+    float rho_hint = 0.0f;
+    if (hint.x > 0.0f) {
+      const float mx = hint.y - prx, my = hint.z - pry;
+      rho_hint = hint.x + sqrtf(mx * mx + my * my) + 1e-3f;
+    }
+    double D = D_fp64;
+    if (SharedPts) {
+      // key bound: |dx_f - dx| <= E; |a - d^2| <= 4 (r + 1) E + 2 E^2 + fl32 rounding
+      const double E = eps_p + fmax(fabs((double)prx - rx), fabs((double)pry - ry)) + K.key_e;
+      D = 4.0 * (radius + 1.0) * E + 2.0 * E * E + D_fp64;
+    }
+    const double rho = hint_radius(rho_hint, radius, D);
+    const float Df = __double2float_ru(D);
+    const SelRange full = range_of(K.r2 + D, Df);
+    const bool restricted = rho < radius;
+    const SelRange R = restricted ? range_of(rho * rho, Df) : full;
+    RowGeo geo{nullptr, prx, pry, (float)cs, (float)inv_cs, 0.0f, nx, ny, 0, 0};
+    geo.init((float)reach);
+    AT.pa[i] = make_float4(prx, pry, geo.marg, Df);
+    AT.pb[i] = make_float4(R.r2hi, R.inv_w, R.two_d, __double2float_rd(K.r2 - D));
+    AT.pc[i] = make_double2(D, rho);
+    AT.pd[i] = make_int4(geo.iy0, geo.nrows, (restricted ? 1 : 0) | (full.beta < 0.125f ? 0 : 2), 0);
+  }
+  // row -> local agent, so the row loop starts from shared memory
+  for (int r = threadIdx.x; r < nrow; r += blockDim.x) AT.rloc[r] = (uint16_t)(T.row_agent[c0 + r] - a0);
   __syncthreads();
   if (SharedPts) mbar_wait(&pts_bar, 0);
-  const double *ax = AT.x, *ay = AT.y, *ah = AT.h, *av = AT.v, *al = AT.l, *aw = AT.w, *ac = AT.c,
-               *as = AT.s;
+  const double *ax = AT.x, *ay = AT.y, *ah = AT.h, *av = AT.v, *ac = AT.c, *as = AT.s;
+  const float *al = AT.l, *aw = AT.w;
+  // the partners' selection parameters are per launch (host)
+  SelParams PP;
+  PP.R = SelRange{K.p_r2hi, K.p_inv_w, 0.0f, K.p_two_d};
+  PP.Df = K.p_Df;
+  PP.r2lo = K.p_r2lo;
+  PP.D = D_fp64;
+  PP.rho = radius;
+  PP.restricted = false;
+  PP.serial = K.p_serial;
 
   for (int r = warp; r < nrow; r += WARPS) {
     const int64_t orow = c0 + r;
@@ -945,43 +1027,37 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     // while the selected road records are in flight
     PartnerSrc psrc{ax, ay, AT.vis, A, i, px, py};
     float no_bound = 0.0f;
-    const int ma = select_topk<true, kEPL>(psrc, cap_a, radius, D_fp64, S, lane, radius, no_bound);
+    const int ma = select_topk<true, kEPL>(psrc, cap_a, radius, PP, S, lane, no_bound);
     int *const psel = reinterpret_cast<int *>(wb + WL.psel);
     for (int m = lane; m < ma; m += 32) psel[m] = S.sel_pl()[m];
     __syncwarp();
 
     // ---- road points: lane l owns cell row iy0 + l of the disc
     int mr = 0;
-    // search hint: (bound on the k-th road distance, position it was taken at)
-    const float4 hint = AT.hint[i];
     float bound = 0.0f;
-    // bound on this step's k-th distance: the hint plus the distance moved
-    // (float; the 1 mm slack exceeds the rounding of the grid-relative floats)
-    float rho_hint = 0.0f;
-    if (hint.x > 0.0f) {
-      const float mx = hint.y - (float)(px - gx0), my = hint.z - (float)(py - gy0);
-      rho_hint = hint.x + sqrtf(mx * mx + my * my) + 1e-3f;
-    }
     if (cap_r > 0) {
-      const double rx = px - gx0, ry = py - gy0;
-      const float prx = (float)rx, pry = (float)ry;
-      RowGeo geo{T.pt_cell_start + cbase, prx, pry, (float)cs, (float)inv_cs, 0.0f, nx, ny, 0, 0};
-      geo.init((float)reach);
+      const float4 pa = AT.pa[i], pb = AT.pb[i];
+      const double2 pc = AT.pc[i];
+      const int4 pd = AT.pd[i];
+      SelParams P;
+      P.R = SelRange{pb.x, pb.y, 0.0f, pb.z};
+      P.Df = pa.w;
+      P.r2lo = pb.w;
+      P.D = pc.x;
+      P.rho = pc.y;
+      P.restricted = pd.z & 1;
+      P.serial = pd.z & 2;
+      const RowGeo geo{T.pt_cell_start + cbase, pa.x, pa.y, (float)cs, (float)inv_cs, pa.z, nx, ny, pd.x, pd.y};
       if (SharedPts) {
-        // key bound: |dx_f - dx| <= E; |a - d^2| <= 4 (r + 1) E + 2 E^2 + fl32 rounding
-        const double E = eps_p + fmax(fabs((double)prx - rx), fabs((double)pry - ry)) + K.key_e;
-        const double D = 4.0 * (radius + 1.0) * E + 2.0 * E * E + D_fp64;
-        const double rho = hint_radius(rho_hint, radius, D);
-        RoadSrcShared rsrc{pts, static_cast<const ds_point_rec *>(T.gpt_rec), (int)p0, prx, pry, px,
+        RoadSrcShared rsrc{pts, static_cast<const ds_point_rec *>(T.gpt_rec), (int)p0, pa.x, pa.y, px,
                            py, &geo, reinterpret_cast<int *>(wb + WL.fr)};
-        rsrc.cover(rho < radius ? rho : reach, lane);
-        mr = select_topk<false, kEPL>(rsrc, cap_r, radius, D, S, lane, rho, bound);
+        rsrc.cover(P.restricted ? P.rho : reach, lane);
+        mr = select_topk<false, kEPL>(rsrc, cap_r, radius, P, S, lane, bound);
       } else {
-        const double rho = hint_radius(rho_hint, radius, D_fp64);
         RoadSrcGlobal rsrc{T.gpt_x, T.gpt_y, T.gpt_id, (int)p0, np, px, py, &geo,
                            reinterpret_cast<int *>(wb + WL.fr)};
-        rsrc.cover(rho < radius ? rho : reach, lane);
-        mr = select_topk<false, kEPL>(rsrc, cap_r, radius, D_fp64, S, lane, rho, bound);
+        rsrc.cover(P.restricted ? P.rho : reach, lane);
+        mr = select_topk<false, kEPL>(rsrc, cap_r, radius, P, S, lane, bound);
       }
     }
     if (St.obs_hint && lane == 0)
@@ -1184,6 +1260,20 @@ cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, void *obs,
   K.cs = h->cfg.grid_cell;
   K.inv_cs = 1.0 / K.cs;
   K.key_e = (K.radius + 1.0) * 1.2e-7;
+  {
+    // float roundings toward +inf (Df) / -inf (r2lo) on the host
+    float Df = (float)K.D_fp64;
+    if ((double)Df < K.D_fp64) Df = nextafterf(Df, INFINITY);
+    float r2lo = (float)(K.r2 - K.D_fp64);
+    if ((double)r2lo > K.r2 - K.D_fp64) r2lo = nextafterf(r2lo, -INFINITY);
+    const SelRange R = range_of(K.r2 + K.D_fp64, Df);
+    K.p_r2hi = R.r2hi;
+    K.p_inv_w = R.inv_w;
+    K.p_two_d = R.two_d;
+    K.p_Df = Df;
+    K.p_r2lo = r2lo;
+    K.p_serial = !(R.beta < 0.125f);
+  }
   const ObsLaunch L{h, K, mask, O, scale, sel_idx, W, fixed, s};
   if (!h->obs_shared_pts) launch_radial<kWarpsGlobal, false>(L);
   else if (h->obs_warps == kWarpsShared) launch_radial<kWarpsShared, true>(L);
