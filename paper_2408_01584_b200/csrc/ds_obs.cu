@@ -123,8 +123,9 @@ __host__ __device__ inline WarpLayout warp_layout(const ds_config &c, bool buffe
 // Per-agent tables staged once per world (structure of arrays):
 //   x, y, heading, speed, cos, sin (f64) | length, width (f32: only their
 //   float32 values are observed) | ego block (7
-//   floats, padded to 8) | road-selection parameters (RoadPre) | flags (u16)
-//   | visible (u8) | row -> local agent (u16)
+//   floats, padded to 8) | road-selection parameters (RoadPre) | partner
+//   key positions (float2, padded to 32) | flags (u16) | row -> local agent
+//   (u16)
 // RoadPre: everything the road selection of one agent needs that does not
 // depend on the candidates, formed by one thread per agent in the prologue
 // (instead of by every lane of the agent's warp):
@@ -141,14 +142,16 @@ struct AgentTabs {
   float4 *pa, *pb;
   double2 *pc;
   int4 *pd;
+  float2 *pxy;
   uint16_t *flg, *rloc;
-  uint8_t *vis;
 };
+
+__host__ __device__ constexpr int pad32(int n) { return (n + 31) & ~31; }
 
 __host__ __device__ inline size_t agents_bytes(int amax) {
   return (size_t)amax * (6 * sizeof(double) + 2 * sizeof(float) + 8 * sizeof(float) +
                          3 * sizeof(float4) + sizeof(double2)) +
-         al16((size_t)amax * sizeof(uint16_t)) * 2 + al16((size_t)amax);
+         (size_t)pad32(amax) * sizeof(float2) + al16((size_t)amax * sizeof(uint16_t)) * 2;
 }
 
 __device__ inline AgentTabs agent_tabs(unsigned char *base, int amax) {
@@ -164,9 +167,9 @@ __device__ inline AgentTabs agent_tabs(unsigned char *base, int amax) {
   t.l = reinterpret_cast<float *>(o); o += (size_t)amax * sizeof(float);
   t.w = reinterpret_cast<float *>(o); o += (size_t)amax * sizeof(float);
   t.ego = reinterpret_cast<float *>(o); o += (size_t)amax * 8 * sizeof(float);
+  t.pxy = reinterpret_cast<float2 *>(o); o += (size_t)pad32(amax) * sizeof(float2);
   t.flg = reinterpret_cast<uint16_t *>(o); o += al16((size_t)amax * sizeof(uint16_t));
-  t.rloc = reinterpret_cast<uint16_t *>(o); o += al16((size_t)amax * sizeof(uint16_t));
-  t.vis = o;
+  t.rloc = reinterpret_cast<uint16_t *>(o);
   return t;
 }
 
@@ -262,25 +265,30 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // reference's distance (glibc hypot port) and the tie-break index.
 // ---------------------------------------------------------------------------
 
-// Agents of the world (partner slots, fp:240-272), FP64 in shared memory.
-// Key: fl32 of an FP64 d^2 -> |a - d^2| <= 2^-22 r2hi.
+// Agents of the world (partner slots, fp:240-272): keys from float2
+// positions relative to the grid origin (shared memory, padded to a whole
+// number of warps; absent / removed agents and the padding hold a far
+// sentinel whose key is +inf), exact distances from the FP64 tables.
+// |a - d^2| <= D as for the road points, with E = both positions' float
+// rounding (the world's largest, measured in the prologue) + the float
+// subtraction.
 struct PartnerSrc {
+  const float2 *pxy;
   const double *x, *y;
-  const uint8_t *vis;
-  int n, self;
+  int npad, self;
+  float prx, pry;
   double px, py;
   __device__ __forceinline__ int pbase() const { return 0; }
   __device__ __forceinline__ bool small_payload() const { return true; }
   template <class F>
   __device__ __forceinline__ void visit(float r2hi, int lane, F &&fn) const {
     #pragma unroll 1
-    for (int f0 = 0; f0 < n; f0 += 32) {
+    for (int f0 = 0; f0 < npad; f0 += 32) {
       const int f = f0 + lane;
-      const int fs = f < n ? f : n - 1;   // branch-free: every lane computes a key
-      const double dx = x[fs] - px, dy = y[fs] - py;
-      const float a = (float)fma(dx, dx, dy * dy);
-      const bool ok = f < n && f != self && vis[fs] && a <= r2hi;
-      fn(ok, a, f);
+      const float2 q = pxy[f];
+      const float dx = q.x - prx, dy = q.y - pry;
+      const float a = fmaf(dx, dx, dy * dy);
+      fn(f != self && a <= r2hi, a, f);
     }
   }
   __device__ __forceinline__ double exact(int pl, int &id) const {
@@ -846,9 +854,6 @@ __device__ int select_topk(Src src, int k, double radius, const SelParams &P, co
 // keeping (or rematerialising) them in registers.
 struct RadialK {
   double radius, reach, r2, D_fp64, cs, inv_cs, key_e;
-  // the partners' selection parameters (SelParams of the full disc)
-  float p_r2hi, p_inv_w, p_two_d, p_Df, p_r2lo;
-  bool p_serial;
 };
 
 template <int WARPS, bool SharedPts, int CAPA, int CAPR>
@@ -867,6 +872,7 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   const int np = (int)(p1 - p0);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t pts_bar;
+  __shared__ float e_max_w[WARPS];   // per warp: largest float rounding of an agent position
   constexpr bool kFixed = CAPA > 0;
   // G positions per lane in the sort (even; runtime caps <= kSelCap: 6)
   constexpr int kEPL = kFixed ? ((gcap_of(CAPA, CAPR) + 63) / 64) * 2 : 2 * ((kSelCap + 48 + 63) / 64);
@@ -936,6 +942,7 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   // agent tables, the ego block of every agent (fp:228-238), the search
   // hints and the road-selection parameters: one thread per agent,
   // overlapping the points' bulk copy
+  float e_own = 0.0f;
   for (int i = threadIdx.x; i < A; i += blockDim.x) {
     const int64_t g = a0 + i;
     const double px = St.x[g], py = St.y[g], hd = St.heading[g], v = St.speed[g];
@@ -949,7 +956,6 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     AT.x[i] = px; AT.y[i] = py; AT.h[i] = hd; AT.v[i] = v;
     AT.l[i] = (float)ln; AT.w[i] = (float)wd; AT.c[i] = ch; AT.s[i] = sh;
     AT.flg[i] = f;
-    AT.vis[i] = (f & DS_F_PRESENT) && !(f & DS_F_REMOVED);
     float *e = AT.ego + 8 * i;
     e[0] = (float)v;
     e[1] = (float)ln;
@@ -985,22 +991,38 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     AT.pb[i] = make_float4(R.r2hi, R.inv_w, R.two_d, __double2float_rd(K.r2 - D));
     AT.pc[i] = make_double2(D, rho);
     AT.pd[i] = make_int4(geo.iy0, geo.nrows, (restricted ? 1 : 0) | (full.beta < 0.125f ? 0 : 2), 0);
+    // partner key position: absent / removed agents get the far sentinel
+    const bool vis = (f & DS_F_PRESENT) && !(f & DS_F_REMOVED);
+    AT.pxy[i] = vis ? make_float2(prx, pry) : make_float2(1e30f, 1e30f);
+    e_own = fmaxf(e_own, (float)fmax(fabs((double)prx - rx), fabs((double)pry - ry)) * (1.0f + 1e-6f));
   }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) e_own = fmaxf(e_own, __shfl_xor_sync(kFull, e_own, off));
+  if (lane == 0) e_max_w[warp] = e_own;
+  for (int i = A + (int)threadIdx.x; i < pad32(A); i += blockDim.x) AT.pxy[i] = make_float2(1e30f, 1e30f);
   // row -> local agent, so the row loop starts from shared memory
   for (int r = threadIdx.x; r < nrow; r += blockDim.x) AT.rloc[r] = (uint16_t)(T.row_agent[c0 + r] - a0);
   __syncthreads();
   if (SharedPts) mbar_wait(&pts_bar, 0);
   const double *ax = AT.x, *ay = AT.y, *ah = AT.h, *av = AT.v, *ac = AT.c, *as = AT.s;
   const float *al = AT.l, *aw = AT.w;
-  // the partners' selection parameters are per launch (host)
+  // the partners' selection parameters (per world): E = both positions'
+  // float rounding + the float subtraction
   SelParams PP;
-  PP.R = SelRange{K.p_r2hi, K.p_inv_w, 0.0f, K.p_two_d};
-  PP.Df = K.p_Df;
-  PP.r2lo = K.p_r2lo;
-  PP.D = D_fp64;
-  PP.rho = radius;
-  PP.restricted = false;
-  PP.serial = K.p_serial;
+  {
+    float em = lane < WARPS ? e_max_w[lane] : 0.0f;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) em = fmaxf(em, __shfl_xor_sync(kFull, em, off));
+    const double E = 2.0 * (double)em + K.key_e;
+    const double D = 4.0 * (radius + 1.0) * E + 2.0 * E * E + D_fp64;
+    PP.Df = __double2float_ru(D);
+    PP.r2lo = __double2float_rd(K.r2 - D);
+    PP.R = range_of(K.r2 + D, PP.Df);
+    PP.D = D;
+    PP.rho = radius;
+    PP.restricted = false;
+    PP.serial = !(PP.R.beta < 0.125f);
+  }
 
   for (int r = warp; r < nrow; r += WARPS) {
     const int64_t orow = c0 + r;
@@ -1025,18 +1047,19 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
 
     // ---- partners: the picks are kept aside (psel); their slots are formed
     // while the selected road records are in flight
-    PartnerSrc psrc{ax, ay, AT.vis, A, i, px, py};
+    const float4 pa = AT.pa[i];
+    PartnerSrc psrc{AT.pxy, ax, ay, pad32(A), i, pa.x, pa.y, px, py};
     float no_bound = 0.0f;
-    const int ma = select_topk<true, kEPL>(psrc, cap_a, radius, PP, S, lane, no_bound);
+    Sel SP = S;                 // the partner picks land in psel
+    SP.L.sel_pl = WL.psel;
+    const int ma = select_topk<true, kEPL>(psrc, cap_a, radius, PP, SP, lane, no_bound);
     int *const psel = reinterpret_cast<int *>(wb + WL.psel);
-    for (int m = lane; m < ma; m += 32) psel[m] = S.sel_pl()[m];
-    __syncwarp();
 
     // ---- road points: lane l owns cell row iy0 + l of the disc
     int mr = 0;
     float bound = 0.0f;
     if (cap_r > 0) {
-      const float4 pa = AT.pa[i], pb = AT.pb[i];
+      const float4 pb = AT.pb[i];
       const double2 pc = AT.pc[i];
       const int4 pd = AT.pd[i];
       SelParams P;
@@ -1260,20 +1283,6 @@ cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, void *obs,
   K.cs = h->cfg.grid_cell;
   K.inv_cs = 1.0 / K.cs;
   K.key_e = (K.radius + 1.0) * 1.2e-7;
-  {
-    // float roundings toward +inf (Df) / -inf (r2lo) on the host
-    float Df = (float)K.D_fp64;
-    if ((double)Df < K.D_fp64) Df = nextafterf(Df, INFINITY);
-    float r2lo = (float)(K.r2 - K.D_fp64);
-    if ((double)r2lo > K.r2 - K.D_fp64) r2lo = nextafterf(r2lo, -INFINITY);
-    const SelRange R = range_of(K.r2 + K.D_fp64, Df);
-    K.p_r2hi = R.r2hi;
-    K.p_inv_w = R.inv_w;
-    K.p_two_d = R.two_d;
-    K.p_Df = Df;
-    K.p_r2lo = r2lo;
-    K.p_serial = !(R.beta < 0.125f);
-  }
   const ObsLaunch L{h, K, mask, O, scale, sel_idx, W, fixed, s};
   if (!h->obs_shared_pts) launch_radial<kWarpsGlobal, false>(L);
   else if (h->obs_warps == kWarpsShared) launch_radial<kWarpsShared, true>(L);
