@@ -147,16 +147,15 @@ __device__ bool offroad_query(const ds_tables &T, const ds_config &C, int w, dou
       // four float prefilter loads in flight, then the tests
       float4 q[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        q[u] = k0 + u < e ? erel[k0 + u] : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+      for (int v = 0; v < 4; ++v)
+        q[v] = k0 + v < e ? erel[k0 + v] : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (fmaxf(q[u].x, q[u].z) < fcx - frx || fminf(q[u].x, q[u].z) > fcx + frx ||
-            fmaxf(q[u].y, q[u].w) < fcy - fry || fminf(q[u].y, q[u].w) > fcy + fry)
+      for (int v = 0; v < 4; ++v) {
+        if (fmaxf(q[v].x, q[v].z) < fcx - frx || fminf(q[v].x, q[v].z) > fcx + frx ||
+            fmaxf(q[v].y, q[v].w) < fcy - fry || fminf(q[v].y, q[v].w) > fcy + fry)
           continue;
-        const int k = k0 + u;
         // FP64 endpoints: one 32-B record (one sector) per entry
-        const double2 *er = reinterpret_cast<const double2 *>(T.eseg_rec) + 2 * (int64_t)k;
+        const double2 *er = reinterpret_cast<const double2 *>(T.eseg_rec) + 2 * (int64_t)(k0 + v);
         const double2 e0 = er[0], e1 = er[1];
         const double ax = e0.x, ay = e0.y, bx = e1.x, by = e1.y;
         // segment AABB vs box AABB (with slack): a superset prefilter
@@ -436,9 +435,12 @@ __global__ void __launch_bounds__(MAXT, MINB) step_kernel(ds_tables T, ds_config
     if (C.collision_behavior == DS_COLL_REMOVE_AGENT && live && (collided || offroad))
       f |= DS_F_PENDING | DS_F_DONE;
   }
-  const int any_end = __syncthreads_or(C.collision_behavior == DS_COLL_END_EPISODE && live &&
-                                        (collided || offroad));
-  bool over = any_end != 0;
+  // the CTA-wide OR only where it decides something (end_episode): other
+  // behaviours let finished warps leave without waiting for the off-road
+  // queries of the rest
+  bool over = false;
+  if (C.collision_behavior == DS_COLL_END_EPISODE)
+    over = __syncthreads_or(live && (collided || offroad)) != 0;
   const int t1 = t + 1;
   if (t1 >= Tw) over = true;
   if (over && ctrl) f |= DS_F_DONE;
