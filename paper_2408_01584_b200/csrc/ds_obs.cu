@@ -631,89 +631,79 @@ struct SelParams {
   bool restricted, serial;
 };
 
-// Exact ascending top-min(n_valid, k) by (distance, id) given candidate keys
-// with |a - d^2| <= D.  Payloads land in S.sel_pl()[0..m).  Warp-collective.
-//  * Direct: small candidate sets (partners) are compacted straight into G
-//    and ranked by counting; a larger set takes the histogram path.
-//  * rho: the radius the source currently covers (< radius when the caller
-//    narrowed it with a search hint, see hint_radius).  A narrowed pass 1 is
-//    used only if every bucket the selection touches provably lies inside
-//    the disc ((bmax + 1) w + D <= rho^2), else it reruns on the full radius.
-//    On return, bound_out holds a bound on the k-th distance (0 when fewer
-//    than k candidates exist).
-//  * ranking uses the float keys: two keys more than 2D apart are ordered
-//    exactly as the distances, so the exact FP64 hypot is evaluated only for
-//    near ties (|a_p - a_q| <= 2D) and possible out-of-radius keys.
-//  * pass 1 keeps (key, payload) in shared memory when they fit.
-template <bool Direct, int EPL, class Src>
-__device__ int select_topk(Src src, int k, double radius, const SelParams &P, const Sel &S,
-                           int lane, float &bound_out) {
-  if (k <= 0) return 0;
-  const double r2 = radius * radius, D = P.D, rho = P.rho;
-  const float Df = P.Df, r2lo = P.r2lo;
-  float r2hi = P.R.r2hi, inv_w = P.R.inv_w, two_d = P.R.two_d;
-  auto set_full = [&]() {
+// The selection's current histogram range (the first one of SelParams, or
+// the full disc after a failed narrowing).
+struct SelState {
+  float r2hi, inv_w, two_d;
+  __device__ __forceinline__ void set_full(double r2, double D, float Df) {
     const SelRange F = range_of(r2 + D, Df);
     r2hi = F.r2hi;
     inv_w = F.inv_w;
     two_d = F.two_d;
-  };
-  if (P.serial) {
-    OBS_STAT(3, 1);
-    set_full();
-    return select_serial(src, k, radius, r2hi, S, lane);
   }
-  if (Direct) {
-    int n = 0;
-    src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
-      const unsigned bal = __ballot_sync(kFull, ok);
-      const int pos = n + __popc(bal & ((1u << lane) - 1u));
-      if (ok && pos < S.gcap) {
-        S.ga()[pos] = a;
-        S.gpl()[pos] = pl;
-      }
-      n += __popc(bal);
-    });
-    bound_out = 0.0f;
-    if (n == 0) return 0;
-    __syncwarp();
-    if (n <= 32) {
-      // one candidate per lane, ranked by counting (key, payload) order over
-      // the n broadcast keys; keys more than 2D apart order exactly like the
-      // distances, so the ranks are the reference's unless a near tie or a
-      // possibly-out-of-radius key sits inside the first k (then the exact
-      // ranking below decides)
-      const float a = lane < n ? S.ga()[lane] : INFINITY;
-      const int pl = lane < n ? S.gpl()[lane] : 0x7fffffff;
-      // (key, payload) order = (key bits, lane): G was compacted in visit
-      // order, so payloads ascend with the lane.  One 32-bit shuffle per
-      // broadcast key (non-negative floats order like their bit patterns);
-      // equal keys are ranked by lane with one match.
-      const unsigned ab = __float_as_uint(a);
-      int rank = __popc(__match_any_sync(kFull, ab) & ((1u << lane) - 1u));
+};
+
+// Small candidate sets (partners): compacted straight into G in visit order
+// and ranked by counting; returns -1 when this fast path cannot decide (more
+// than 32 candidates, or a near tie / a possibly-out-of-radius key among the
+// first k).
+template <class Src>
+__device__ __forceinline__ int select_direct(const Src &src, int k, const SelParams &P,
+                                             const SelState &R, const Sel &S, int lane,
+                                             float &bound_out) {
+  int n = 0;
+  src.visit(R.r2hi, lane, [&](bool ok, float a, int pl) {
+    const unsigned bal = __ballot_sync(kFull, ok);
+    const int pos = n + __popc(bal & ((1u << lane) - 1u));
+    if (ok && pos < S.gcap) {
+      S.ga()[pos] = a;
+      S.gpl()[pos] = pl;
+    }
+    n += __popc(bal);
+  });
+  bound_out = 0.0f;
+  if (n == 0) return 0;
+  if (n > 32) return -1;
+  __syncwarp();
+  // one candidate per lane, ranked by counting (key, payload) order over the
+  // n broadcast keys; keys more than 2D apart order exactly like the
+  // distances.  (key, payload) order = (key bits, lane): G was compacted in
+  // visit order, so payloads ascend with the lane.  One 32-bit shuffle per
+  // broadcast key (non-negative floats order like their bit patterns); equal
+  // keys are ranked by lane with one match.
+  const float a = lane < n ? S.ga()[lane] : INFINITY;
+  const int pl = lane < n ? S.gpl()[lane] : 0x7fffffff;
+  const unsigned ab = __float_as_uint(a);
+  int rank = __popc(__match_any_sync(kFull, ab) & ((1u << lane) - 1u));
 #pragma unroll 4
-      for (int j = 0; j < n; ++j) rank += __shfl_sync(kFull, ab, j) < ab ? 1 : 0;
-      // near ties between sorted neighbours, staged in the idle pass-1 buffer
-      float *const srt = S.ca();
-      if (lane < n) srt[rank] = a;
-      __syncwarp();
-      bool amb = false;
-      if (lane < n)
-        amb = (rank + 1 < n && srt[rank + 1] - a <= two_d) || (rank > 0 && a - srt[rank - 1] <= two_d);
-      const bool bad = lane < n && rank < k && (amb || a > r2lo);
-      if (!__any_sync(kFull, bad)) {
-        if (lane < n && rank < k) S.sel_pl()[rank] = pl;
-        __syncwarp();
-        return n < k ? n : k;
-      }
-    }
-    OBS_STAT(6, 1);
-    if (n <= S.gcap) {
-      // one block in visit order: n transposition rounds
-      return rank_set<EPL>(src, n, n, two_d, r2lo, radius, k, S, lane);
-    }
-    __syncwarp();
-  }
+  for (int j = 0; j < n; ++j) rank += __shfl_sync(kFull, ab, j) < ab ? 1 : 0;
+  // near ties between sorted neighbours, staged in the idle pass-1 buffer
+  float *const srt = S.ca();
+  if (lane < n) srt[rank] = a;
+  __syncwarp();
+  bool amb = false;
+  if (lane < n)
+    amb = (rank + 1 < n && srt[rank + 1] - a <= R.two_d) || (rank > 0 && a - srt[rank - 1] <= R.two_d);
+  const bool bad = lane < n && rank < k && (amb || a > P.r2lo);
+  if (__any_sync(kFull, bad)) return -1;
+  if (lane < n && rank < k) S.sel_pl()[rank] = pl;
+  __syncwarp();
+  return n < k ? n : k;
+}
+
+// Larger sets (road points): histogram threshold, counting-sort scatter into
+// G, rank_set.  Returns -1 when G would exceed its capacity.
+//  * rho: the radius the source currently covers (< radius when the caller
+//    narrowed it with a search hint, see hint_radius).  A narrowed pass 1 is
+//    used only if every bucket the selection touches provably lies inside
+//    the disc ((bmax + 1) w + D <= rho^2), else it reruns on the full radius.
+//    bound_out: a bound on the k-th distance (0 when fewer than k candidates
+//    exist).
+//  * pass 1 keeps (key, payload) in shared memory when they fit.
+template <int EPL, class Src>
+__device__ __forceinline__ int select_hist(Src &src, int k, double radius, const SelParams &P,
+                                           SelState &R, const Sel &S, int lane, float &bound_out) {
+  const double r2 = radius * radius, D = P.D, rho = P.rho;
   bool restricted = P.restricted;
   const int pb = src.pbase();
   const bool small = src.small_payload();
@@ -730,7 +720,8 @@ __device__ int select_topk(Src src, int k, double radius, const SelParams &P, co
     for (int v = 0; v < kVec; ++v) hc4[lane + 32 * v] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
     nbuf = 0;
-    src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
+    const float inv_w = R.inv_w;
+    src.visit(R.r2hi, lane, [&](bool ok, float a, int pl) {
       // branch-free: a lane without a candidate adds 0 (its key is finite
       // and >= 0, so its bucket index is in range)
       atomicAdd(&S.hc()[bucket_of(a, inv_w)], ok ? 1u : 0u);
@@ -743,12 +734,10 @@ __device__ int select_topk(Src src, int k, double radius, const SelParams &P, co
       nbuf += __popc(bal);
     });
     __syncwarp();
-    {
 #pragma unroll
-      for (int v = 0; v < kVec; ++v) {
-        const uint4 c = hc4[kVec * lane + v];
-        cnt[4 * v] = c.x; cnt[4 * v + 1] = c.y; cnt[4 * v + 2] = c.z; cnt[4 * v + 3] = c.w;
-      }
+    for (int v = 0; v < kVec; ++v) {
+      const uint4 c = hc4[kVec * lane + v];
+      cnt[4 * v] = c.x; cnt[4 * v + 1] = c.y; cnt[4 * v + 2] = c.z; cnt[4 * v + 3] = c.w;
     }
     local = 0;
 #pragma unroll
@@ -769,23 +758,22 @@ __device__ int select_topk(Src src, int k, double radius, const SelParams &P, co
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) bstar = min(bstar, __shfl_xor_sync(kFull, bstar, off));
-    // G = buckets <= b*+1: an element of b*+1 reaches rank < k only through an
-    // inversion with b* at their shared edge, and its window never needs
-    // b*+2 (all of b*+2 lies above it); edge windows are clamped to bmax
+    // G = buckets <= b*+1: an element of b*+2 has at least k elements
+    // exactly nearer (all of buckets <= b*), so it never ranks below k
     bmax = min(bstar + 1, kNB - 1);
-    w = (double)r2hi / kNB;
+    w = (double)R.r2hi / kNB;
     // a narrowed scan is valid only if all buckets <= bmax lie inside the disc
     OBS_STAT(1, total);
     if (restricted && !((((double)bmax + 1.01) * w + D) <= rho * rho)) {
       OBS_STAT(2, 1);
       src.restrict_to(radius + 1e-6, lane);
       restricted = false;
-      set_full();
+      R.set_full(r2, D, P.Df);
       continue;
     }
     break;
   }
-  bound_out = total >= (uint32_t)k ? sqrtf(((float)bstar + 1.0f) * (float)w + Df) * (1.0f + 1e-6f)
+  bound_out = total >= (uint32_t)k ? sqrtf(((float)bstar + 1.0f) * (float)w + P.Df) * (1.0f + 1e-6f)
                                     : 0.0f;
   if (total == 0) return 0;
   uint32_t run2 = incl - local;
@@ -803,19 +791,16 @@ __device__ int select_topk(Src src, int k, double radius, const SelParams &P, co
     const uint32_t hb = S.hc()[bmax];   // (start << 16) | count of the last kept bucket
     n_g = (hb >> 16) + (hb & 0xffffu);
   }
+  if (n_g > (uint32_t)S.gcap || total > 0xffffu) return -1;
   // largest kept bucket: the sort's round count
   int cmax = 0;
 #pragma unroll
   for (int q = 0; q < kPer; ++q)
     if (lane * kPer + q <= bmax) cmax = max(cmax, (int)cnt[q]);
   cmax = (int)__reduce_max_sync(kFull, (unsigned)cmax);
-  if (n_g > (uint32_t)S.gcap || total > 0xffffu) {
-    OBS_STAT(3, 1);
-    src.restrict_to(radius + 1e-6, lane);
-    return select_serial(src, k, radius, r2hi, S, lane);
-  }
   OBS_STAT(4, n_g);
   // pass 2: counting-sort scatter of buckets <= bmax into G
+  const float inv_w = R.inv_w;
   auto scatter = [&](float a, int pl) {
     const int b = bucket_of(a, inv_w);
     if (b <= bmax) {
@@ -836,12 +821,40 @@ __device__ int select_topk(Src src, int k, double radius, const SelParams &P, co
     OBS_STAT(7, 1);
     // only keys in buckets <= bmax matter: a < (bmax + 1) w, so d^2 < that + D
     if (bmax < kNB - 1) src.restrict_to(sqrt(((double)bmax + 1.01) * w + D) + 1e-6, lane);
-    src.visit(r2hi, lane, [&](bool ok, float a, int pl) {
+    src.visit(R.r2hi, lane, [&](bool ok, float a, int pl) {
       if (ok) scatter(a, pl);
     });
   }
   __syncwarp();
-  return rank_set<EPL>(src, (int)n_g, cmax, two_d, r2lo, radius, k, S, lane);
+  return rank_set<EPL>(src, (int)n_g, cmax, R.two_d, P.r2lo, radius, k, S, lane);
+}
+
+// Exact ascending top-min(n_valid, k) by (distance, id) given candidate keys
+// with |a - d^2| <= D.  Payloads land in S.sel_pl()[0..m).  Warp-collective.
+// Direct: the partners' counting path, else the histogram path; ranking uses
+// the float keys (two keys more than 2D apart are ordered exactly as the
+// distances), the exact FP64 hypot only near ties and the radius.  Either
+// path falls back to the reference's serial insertion -- exact by
+// construction, one call site (code size) -- for a loose key bound
+// (P.serial), a set the fast path cannot rank, or a G beyond capacity.
+template <bool Direct, int EPL, class Src>
+__device__ int select_topk(Src src, int k, double radius, const SelParams &P, const Sel &S,
+                           int lane, float &bound_out) {
+  if (k <= 0) return 0;
+  SelState R{P.R.r2hi, P.R.inv_w, P.R.two_d};
+  if (!P.serial) {
+    int m;
+    if constexpr (Direct) m = select_direct(src, k, P, R, S, lane, bound_out);
+    else m = select_hist<EPL>(src, k, radius, P, R, S, lane, bound_out);
+    if (m >= 0) return m;
+    OBS_STAT(Direct ? 6 : 3, 1);
+  } else {
+    OBS_STAT(3, 1);
+  }
+  __syncwarp();
+  R.set_full(radius * radius, P.D, P.Df);
+  src.restrict_to(radius + 1e-6, lane);
+  return select_serial(src, k, radius, R.r2hi, S, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -1024,6 +1037,8 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     PP.serial = !(PP.R.beta < 0.125f);
   }
 
+  // float32 rows without normalisation leave by bulk stores
+  const bool bulk_out = O.dtype == DS_OBS_F32 && scale == nullptr;
   for (int r = warp; r < nrow; r += WARPS) {
     const int64_t orow = c0 + r;
     const int i = AT.rloc[r];
@@ -1038,6 +1053,11 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
       continue;
     }
     OBS_STAT(0, 1);
+    if (bulk_out) {
+      // the previous row's bulk store must have read the staging buffer
+      if (lane == 0) bulk_row_wait();
+      __syncwarp();
+    }
     // the staged row copies the output row's 16-B phase (vector write-out)
     const int out_phase = out_row_phase(O, orow);
     float *const row = row0 - ((row0_phase - out_phase) & 3);   // contiguous staged row
@@ -1170,9 +1190,14 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     }
     __syncwarp();
     // ---- coalesced write-out of the staged row
-    write_row(O, orow, row, obs_width, scale, lane);
-    __syncwarp();
+    if (bulk_out) {
+      write_row_bulk(O, orow, row, obs_width, lane);
+    } else {
+      write_row(O, orow, row, obs_width, scale, lane);
+      __syncwarp();
+    }
   }
+  if (bulk_out && lane == 0) bulk_row_wait();   // the staging must outlive the copies
 }
 
 #ifdef DS_OBS_STATS

@@ -33,6 +33,44 @@ __device__ __forceinline__ float scaled(const float *row, const float *scale, in
   return scale ? __fdiv_rn(row[c], scale[c]) : row[c];
 }
 
+// Bulk (TMA engine) shared -> global store of a staged row's 16-B aligned
+// body: one instruction of one lane instead of a load / store per float4.
+// The issuing lane must wait for the source to be read (bulk_row_wait)
+// before the staging buffer is written again, and before the CTA exits.
+__device__ __forceinline__ void bulk_row_store(float *gdst, const float *ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"((uint32_t)__cvta_generic_to_shared(ssrc)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_row_wait() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// Warp-collective float32 write-out of a staged row whose 16-B phase matches
+// the output row's, without normalisation: head / tail floats by single
+// stores of lanes 0-3 / 4-7, the aligned body by one bulk store of lane 0
+// (call bulk_row_wait on lane 0 before reusing `row`).
+__device__ __forceinline__ void write_row_bulk(const ObsOut &o, int64_t orow, const float *row,
+                                               int width, int lane) {
+  float *out = static_cast<float *>(o.base) + orow * (int64_t)o.stride;
+  const int ph = (int)((reinterpret_cast<uintptr_t>(out) >> 2) & 3);
+  const int head = min((4 - ph) & 3, width);
+  const int nvec = (width - head) >> 2;
+  const int tail0 = head + 4 * nvec;
+  const int c = lane < 4 ? lane : tail0 + lane - 4;
+  if (lane < 4 ? lane < head : (lane < 8 && c < width)) out[c] = row[c];
+  // the staged row was written through the generic proxy: every writer
+  // fences toward the async proxy, then one lane issues the copy
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0 && nvec > 0) bulk_row_store(out + head, row + head, (uint32_t)nvec * 16u);
+  if (o.stride > width) {
+#pragma unroll 1
+    for (int q = width + lane; q < o.stride; q += 32) out[q] = 0.0f;
+  }
+}
+
 // Warp-collective: row[0, width) (divided by scale[c] when scale != NULL) to
 // output row orow, zeros in [width, stride).
 __device__ __forceinline__ void write_row(const ObsOut &o, int64_t orow, const float *row,
