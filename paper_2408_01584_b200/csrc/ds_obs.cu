@@ -315,6 +315,10 @@ struct RoadSrcShared {
     geo->range((float)rho, lane, b, c);
     rows.build(b - p0, c, lane, fscr);
   }
+  // cover() from the raw cell-table values of GeoRow::range_issue
+  __device__ __forceinline__ void cover_raw(int v0, int v1, int lane) {
+    rows.build(v0 - p0, v1 - v0, lane, fscr);
+  }
   __device__ __forceinline__ void restrict_to(double rho, int lane) { cover(rho, lane); }
   __device__ __forceinline__ int pbase() const { return 0; }
   __device__ __forceinline__ bool small_payload() const { return true; }
@@ -1063,38 +1067,40 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     float *const row = row0 - ((row0_phase - out_phase) & 3);   // contiguous staged row
     const double px = ax[i], py = ay[i], h = ah[i];
     const double ch = ac[i], sh = as[i];
-    if (lane < 7) row[lane] = AT.ego[8 * i + lane];   // ego block, formed in the prologue
+    const float4 pa = AT.pa[i], pb = AT.pb[i];
+    const double2 pc = AT.pc[i];
+    const int4 pd = AT.pd[i];
+    SelParams P;
+    P.R = SelRange{pb.x, pb.y, 0.0f, pb.z};
+    P.Df = pa.w;
+    P.r2lo = pb.w;
+    P.D = pc.x;
+    P.rho = pc.y;
+    P.restricted = pd.z & 1;
+    P.serial = pd.z & 2;
+    const RowGeo geo{T.pt_cell_start + cbase, pa.x, pa.y, (float)cs, (float)inv_cs, pa.z, nx, ny, pd.x, pd.y};
+    // the road rows' cell-table loads stay in flight across the partners
+    int rv0 = 0, rv1 = 0;
+    if (SharedPts && cap_r > 0) geo.range_issue((float)(P.restricted ? P.rho : reach), lane, rv0, rv1);
 
     // ---- partners: the picks are kept aside (psel); their slots are formed
     // while the selected road records are in flight
-    const float4 pa = AT.pa[i];
+    Sel SP = S;
+    SP.L.sel_pl = WL.psel;
     PartnerSrc psrc{AT.pxy, ax, ay, pad32(A), i, pa.x, pa.y, px, py};
     float no_bound = 0.0f;
-    Sel SP = S;                 // the partner picks land in psel
-    SP.L.sel_pl = WL.psel;
     const int ma = select_topk<true, kEPL>(psrc, cap_a, radius, PP, SP, lane, no_bound);
     int *const psel = reinterpret_cast<int *>(wb + WL.psel);
+    if (lane < 7) row[lane] = AT.ego[8 * i + lane];   // ego block, formed in the prologue
 
     // ---- road points: lane l owns cell row iy0 + l of the disc
     int mr = 0;
     float bound = 0.0f;
     if (cap_r > 0) {
-      const float4 pb = AT.pb[i];
-      const double2 pc = AT.pc[i];
-      const int4 pd = AT.pd[i];
-      SelParams P;
-      P.R = SelRange{pb.x, pb.y, 0.0f, pb.z};
-      P.Df = pa.w;
-      P.r2lo = pb.w;
-      P.D = pc.x;
-      P.rho = pc.y;
-      P.restricted = pd.z & 1;
-      P.serial = pd.z & 2;
-      const RowGeo geo{T.pt_cell_start + cbase, pa.x, pa.y, (float)cs, (float)inv_cs, pa.z, nx, ny, pd.x, pd.y};
       if (SharedPts) {
         RoadSrcShared rsrc{pts, static_cast<const ds_point_rec *>(T.gpt_rec), (int)p0, pa.x, pa.y, px,
                            py, &geo, reinterpret_cast<int *>(wb + WL.fr)};
-        rsrc.cover(P.restricted ? P.rho : reach, lane);
+        rsrc.cover_raw(rv0, rv1, lane);
         mr = select_topk<false, kEPL>(rsrc, cap_r, radius, P, S, lane, bound);
       } else {
         RoadSrcGlobal rsrc{T.gpt_x, T.gpt_y, T.gpt_id, (int)p0, np, px, py, &geo,

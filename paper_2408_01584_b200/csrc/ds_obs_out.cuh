@@ -47,6 +47,7 @@ __device__ __forceinline__ void bulk_row_wait() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
+
 // Warp-collective float32 write-out of a staged row whose 16-B phase matches
 // the output row's, without normalisation: head / tail floats by single
 // stores of lanes 0-3 / 4-7, the aligned body by one bulk store of lane 0
