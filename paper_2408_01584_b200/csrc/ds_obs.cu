@@ -956,31 +956,38 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   const double eps_p = SharedPts ? T.grid_eps[w] : 0.0;
   const double D_fp64 = K.D_fp64;       // fl32 of an FP64 d^2
 
-  // agent tables, the ego block of every agent (fp:228-238), the search
-  // hints and the road-selection parameters: one thread per agent,
-  // overlapping the points' bulk copy
+  // agent tables and the ego block of every agent (fp:228-238), then -- by
+  // a second group of threads -- the road-selection parameters and partner
+  // key positions: one thread per (agent, part), overlapping the points'
+  // bulk copy (the two parts split the prologue's critical path)
   float e_own = 0.0f;
-  for (int i = threadIdx.x; i < A; i += blockDim.x) {
+  for (int u = threadIdx.x; u < 2 * A; u += blockDim.x) {
+    const bool tabs = u < A;
+    const int i = tabs ? u : u - A;
     const int64_t g = a0 + i;
-    const double px = St.x[g], py = St.y[g], hd = St.heading[g], v = St.speed[g];
-    const double ln = T.length[g], wd = T.width[g];
-    const double gx = T.goal_x[g] - px, gy = T.goal_y[g] - py;
+    const double px = St.x[g], py = St.y[g];
     const uint16_t f = St.flags[g];
+    if (tabs) {
+      const double hd = St.heading[g], v = St.speed[g];
+      const double ln = T.length[g], wd = T.width[g];
+      const double gx = T.goal_x[g] - px, gy = T.goal_y[g] - py;
+      double sh, ch;
+      sincos(hd, &sh, &ch);
+      AT.x[i] = px; AT.y[i] = py; AT.h[i] = hd; AT.v[i] = v;
+      AT.l[i] = (float)ln; AT.w[i] = (float)wd; AT.c[i] = ch; AT.s[i] = sh;
+      AT.flg[i] = f;
+      float *e = AT.ego + 8 * i;
+      e[0] = (float)v;
+      e[1] = (float)ln;
+      e[2] = (float)wd;
+      e[3] = (float)(gx * ch + gy * sh);
+      e[4] = (float)(gy * ch - gx * sh);
+      e[5] = (float)hypot(gx, gy);
+      e[6] = (f & DS_F_COLLIDED) ? 1.0f : 0.0f;
+      continue;
+    }
     const float4 hint = St.obs_hint ? reinterpret_cast<const float4 *>(St.obs_hint)[g]
                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-    double sh, ch;
-    sincos(hd, &sh, &ch);
-    AT.x[i] = px; AT.y[i] = py; AT.h[i] = hd; AT.v[i] = v;
-    AT.l[i] = (float)ln; AT.w[i] = (float)wd; AT.c[i] = ch; AT.s[i] = sh;
-    AT.flg[i] = f;
-    float *e = AT.ego + 8 * i;
-    e[0] = (float)v;
-    e[1] = (float)ln;
-    e[2] = (float)wd;
-    e[3] = (float)(gx * ch + gy * sh);
-    e[4] = (float)(gy * ch - gx * sh);
-    e[5] = (float)hypot(gx, gy);
-    e[6] = (f & DS_F_COLLIDED) ? 1.0f : 0.0f;
     // road selection: the bound on this step's k-th distance is the hint
     // plus the distance moved (float; the 1 mm slack exceeds the rounding of
     // the grid-relative floats)
