@@ -16,6 +16,8 @@
 
 namespace ds {
 
+constexpr int kStepBins = 64;   // x-bins of the agent-agent sweep
+
 struct StepShared {
   double *x, *y, *c, *s, *hl, *hw, *cr;
   uint8_t *elig;
@@ -23,10 +25,11 @@ struct StepShared {
   // circumcircle prefilter: float position relative to the world's grid
   // origin, circumradius padded by the float rounding bound (> 0: eligible)
   float4 *pre;
-  // sweep-and-prune order: left edges of the padded circles' x-intervals
-  // (+inf: not eligible) and agent ids, sorted ascending over sort_n slots
+  // sweep-and-prune order: the eligible agents' ids (sord) and x-bins (skey,
+  // as int), counting-sorted by bin
   float *skey;
   int *sord;
+  int *bcnt, *bstart;   // x-bin counts / starts (+ total) of the sweep
 };
 
 __host__ __device__ inline int pow2_at_least(int n) {
@@ -51,12 +54,15 @@ __device__ __forceinline__ StepShared carve_step(void *base, int amax) {
       (reinterpret_cast<uintptr_t>(sh.hit + amax) + 15) & ~uintptr_t(15));
   sh.skey = reinterpret_cast<float *>(sh.pre + amax);
   sh.sord = reinterpret_cast<int *>(sh.skey + pow2_at_least(amax));
+  sh.bcnt = sh.sord + pow2_at_least(amax);
+  sh.bstart = sh.bcnt + kStepBins;
   return sh;
 }
 
 size_t step_smem_bytes(int max_agents) {
   return (size_t)max_agents * (7 * sizeof(double) + 2) + 16 + (size_t)max_agents * sizeof(float4) +
-         (size_t)pow2_at_least(max_agents) * (sizeof(float) + sizeof(int));
+         (size_t)pow2_at_least(max_agents) * (sizeof(float) + sizeof(int)) +
+         (2 * kStepBins + 1) * sizeof(int);
 }
 
 // SAT over the 4 box axes, _fastpath.sat_pairs (fp:29-53); (i, j) with i < j.
@@ -350,53 +356,65 @@ __global__ void __launch_bounds__(MAXT, MINB) step_kernel(ds_tables T, ds_config
     sh.pre[tid] = make_float4(fx, fy, pr, elig ? 1.0f : 0.0f);
     sh.hit[tid] = 0;
   }
+  for (int b0 = tid; b0 < kStepBins; b0 += blockDim.x) sh.bcnt[b0] = 0;
   __syncthreads();
 
   bool collided = false, offroad = false;
-  // Agent-agent pairs by sweep and prune: sort the padded circles' x-intervals
-  // by their left edge (bitonic, ties by id), then each sorted position scans
-  // forward only while the next left edge is inside its own interval -- every
-  // pair whose circles can overlap is tested exactly once, and both ends are
-  // flagged (SAT runs on (min, max) id, so either end computes the same bits).
-  const int sort_n = pow2_at_least(A);
-  for (int e = tid; e < sort_n; e += blockDim.x) {
-    float key = INFINITY;
-    if (e < A) {
-      const float4 pe = sh.pre[e];
-      if (pe.w != 0.0f) key = pe.x - pe.z;
+  // Agent-agent pairs by sweep and prune over x-bins: the eligible agents
+  // are counting-sorted by the bin of their padded circle's left edge (bins
+  // are monotone in x, so every agent after p in this order starts at or
+  // beyond p's bin), then each position scans forward while the next
+  // agent's bin is <= the bin of its own right edge -- every pair whose
+  // circles can overlap is tested exactly once (within a bin, by the earlier
+  // position), and both ends are flagged (SAT runs on (min, max) id, so
+  // either end computes the same bits).  Four barriers instead of a bitonic
+  // network's log^2 stages.
+  const float ext = (float)T.grid_nx[w] * (float)C.grid_cell;
+  const float inv_bw = ext > 0.0f ? (float)kStepBins / ext : 0.0f;
+  auto bin_of = [&](float xr) {
+    return (int)fminf(fmaxf(floorf(xr * inv_bw), 0.0f), (float)(kStepBins - 1));
+  };
+  int my_bin = -1, my_pos = 0;
+  if (act_here) {
+    const float4 pe = sh.pre[tid];
+    if (pe.w != 0.0f) {
+      my_bin = bin_of(pe.x - pe.z);
+      my_pos = atomicAdd(&sh.bcnt[my_bin], 1);
     }
-    sh.skey[e] = key;
-    sh.sord[e] = e;
   }
   __syncthreads();
-  for (int size = 2; size <= sort_n; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int e = tid; e < sort_n; e += blockDim.x) {
-        const int o = e ^ stride;
-        if (o > e) {
-          const float ke = sh.skey[e], ko = sh.skey[o];
-          const int ie = sh.sord[e], io = sh.sord[o];
-          const bool greater = ke > ko || (ke == ko && ie > io);
-          if (greater == ((e & size) == 0)) {
-            sh.skey[e] = ko;
-            sh.skey[o] = ke;
-            sh.sord[e] = io;
-            sh.sord[o] = ie;
-          }
-        }
+  if (tid < 32) {
+    // exclusive scan of the bin counts (one warp)
+    int carry = 0;
+    for (int b0 = 0; b0 < kStepBins; b0 += 32) {
+      const int c = sh.bcnt[b0 + tid];
+      int incl = c;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int up = __shfl_up_sync(0xffffffffu, incl, off);
+        if (tid >= off) incl += up;
       }
-      __syncthreads();
+      sh.bstart[b0 + tid] = carry + incl - c;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
+    if (tid == 0) sh.bstart[kStepBins] = carry;
   }
-  for (int p = tid; p < A; p += blockDim.x) {
-    const float kp = sh.skey[p];
-    if (kp == INFINITY) continue;          // not eligible (sorted last)
+  __syncthreads();
+  if (my_bin >= 0) {
+    const int slot = sh.bstart[my_bin] + my_pos;
+    sh.sord[slot] = tid;
+    reinterpret_cast<int *>(sh.skey)[slot] = my_bin;
+  }
+  __syncthreads();
+  const int n_elig = sh.bstart[kStepBins];
+  const int *sbin = reinterpret_cast<const int *>(sh.skey);
+  for (int p = tid; p < n_elig; p += blockDim.x) {
     const int i = sh.sord[p];
     const float4 pi = sh.pre[i];
-    const float right = pi.x + pi.z + 1e-4f * (1.0f + fabsf(pi.x));
+    const int rbin = bin_of(pi.x + pi.z + 1e-4f * (1.0f + fabsf(pi.x)));
     bool hit_any = false;
-    for (int q = p + 1; q < A; ++q) {
-      if (sh.skey[q] > right) break;       // this and all later intervals start beyond i's
+    for (int q = p + 1; q < n_elig; ++q) {
+      if (sbin[q] > rbin) break;            // this and all later circles start beyond i's
       const int j = sh.sord[q];
       // boxes lie inside their circumcircles: disjoint circles cannot collide
       // (float superset test on padded radii; SAT below decides exactly)
