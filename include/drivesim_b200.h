@@ -148,6 +148,9 @@ typedef struct ds_tables {
   /* the FP64 endpoints of eseg_* as one 32-B record (ax, ay, bx, by) per
    * entry: the off-road slab test's exact phase reads one sector */
   const double *eseg_rec;
+  /* the FP64 endpoints of aseg_* as one 32-B record (ax, ay, bx, by) per
+   * entry: the LiDAR / view-cone segment fetch reads one sector */
+  const double *aseg_rec;
 } ds_tables;
 
 /* One road point of gpt_rec: the gpt_x / gpt_y / gpt_h / gpt_id / gpt_kind

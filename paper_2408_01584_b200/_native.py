@@ -65,7 +65,7 @@ TABLE_PTRS = [
     "p_off", "pt_cell_start", "gpt_x", "gpt_y", "gpt_h", "gpt_kind", "gpt_id",
     "eseg_cell_start", "eseg_ax", "eseg_ay", "eseg_bx", "eseg_by",
     "aseg_cell_start", "aseg_ax", "aseg_ay", "aseg_bx", "aseg_by", "aseg_id", "aseg_edge",
-    "s_off", "gpt_xy", "grid_eps", "gpt_rec", "eseg_rel", "agent_rec", "eseg_rec",
+    "s_off", "gpt_xy", "grid_eps", "gpt_rec", "eseg_rel", "agent_rec", "eseg_rec", "aseg_rec",
 ]
 
 

@@ -455,7 +455,10 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
           const int e = cells.map(f0, lane);
           int k_lo = 0, n_k = 0;
           if (f0 + lane < cells.total) {
-            const double ax = T.aseg_ax[e], ay = T.aseg_ay[e], bx = T.aseg_bx[e], by = T.aseg_by[e];
+            // FP64 endpoints: one 32-B record (one sector)
+            const double2 *sr = reinterpret_cast<const double2 *>(T.aseg_rec) + 2 * (int64_t)e;
+            const double2 ra = sr[0], rb = sr[1];
+            const double ax = ra.x, ay = ra.y, bx = rb.x, by = rb.y;
             seg_ax[lane] = ax;
             seg_ay[lane] = ay;
             seg_bx[lane] = bx;
@@ -506,10 +509,12 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
         // (that ring - 1) cells from the origin's cell
         const int rrem = q0 + 32 < n_cells ? ring_of(q0 + 32) : 0;   // warp-uniform
         if (rrem >= 2) {
-          const double far = (rrem - 1) * cs - 1e-6;
+          // float compare against far rounded down: only ever keeps walking
+          // longer than the FP64 test would (extra cells cannot change hits)
+          const float far = __double2float_rd((rrem - 1) * cs - 1e-6);
           bool open = false;
           #pragma unroll 1
-          for (int k = lane; k < R; k += 32) open = open || !((double)rbf[k] < far);
+          for (int k = lane; k < R; k += 32) open = open || !(rbf[k] < far);
           if (!__any_sync(kFullMask, open)) break;
         }
       }

@@ -334,6 +334,9 @@ class SimBatch:
                               .astype(np.float64).reshape(-1), dev)
         t["eseg_rec"] = _dev(np.stack([lay.eseg_ax, lay.eseg_ay, lay.eseg_bx, lay.eseg_by], 1)
                              .astype(np.float64).reshape(-1), dev)
+        # 32-B FP64 records of all binned segments (LiDAR / view-cone fetch)
+        t["aseg_rec"] = _dev(np.stack([lay.aseg_ax, lay.aseg_ay, lay.aseg_bx, lay.aseg_by], 1)
+                             .astype(np.float64).reshape(-1), dev)
         t["p_off"] = _dev(pw.p_off, dev)
         t["s_off"] = _dev(pw.s_off, dev)
         self._t_tensors = t
