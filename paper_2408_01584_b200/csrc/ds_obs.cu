@@ -48,7 +48,10 @@ constexpr int kCandShared = 224;  // (shared-points variant: hint-narrowed scans
 // warps per world CTA: as many as the shared memory allows (occupancy is what
 // hides this kernel's latencies: 16 / 24 / 28 / 32 warps measured 2.82 /
 // 2.53 / 2.28 / 2.16 ms at C3); 32 fits the default caps with 10k points
-constexpr int kWarpsShared = 32;
+#ifndef DS_OBS_WARPS
+#define DS_OBS_WARPS 32
+#endif
+constexpr int kWarpsShared = DS_OBS_WARPS;
 constexpr int kWarpsSharedSmall = 24;
 // batches of >= 2 x #SMs worlds of <= 64 agents whose tables fit twice per
 // SM: two 16-warp CTAs per SM (the same 32 warps, but one world's staging
@@ -56,7 +59,9 @@ constexpr int kWarpsSharedSmall = 24;
 constexpr int kWarpsSharedPair = 16;
 constexpr int kSmemPerSM = 228 * 1024;
 constexpr int kWarpsGlobal = 12;
-constexpr size_t kStaticSmem = 16;   // the points' mbarrier (static shared memory)
+// static shared memory of the radial kernel (mbarrier, per-warp rounding
+// maxima, row counter): an upper bound for the launch plan
+constexpr size_t kStaticSmem = 256;
 
 __host__ __device__ constexpr int kmax_of(int cap_a, int cap_r) {
   return (cap_a > cap_r ? cap_a : cap_r) < 1 ? 1 : (cap_a > cap_r ? cap_a : cap_r);
@@ -890,6 +895,7 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t pts_bar;
   __shared__ float e_max_w[WARPS];   // per warp: largest float rounding of an agent position
+  __shared__ int next_row;           // rows are handed out dynamically (no tail imbalance)
   constexpr bool kFixed = CAPA > 0;
   // G positions per lane in the sort (even; runtime caps <= kSelCap: 6)
   constexpr int kEPL = kFixed ? ((gcap_of(CAPA, CAPR) + 63) / 64) * 2 : 2 * ((kSelCap + 48 + 63) / 64);
@@ -918,6 +924,7 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   // copy, an odd head / tail point by plain loads; pts[j] = point p0 + j
   float2 *const pbuf = reinterpret_cast<float2 *>(after_scratch);
   float2 *const pts = pbuf + (p0 & 1);
+  if (threadIdx.x == 0) next_row = WARPS;   // rows 0..WARPS-1 start statically
   if (SharedPts && threadIdx.x == 0) {
     mbar_init(&pts_bar, 1);
     const int64_t pa = (p0 + 1) & ~int64_t(1), pb = p1 & ~int64_t(1);
@@ -1050,7 +1057,12 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
 
   // float32 rows without normalisation leave by bulk stores
   const bool bulk_out = O.dtype == DS_OBS_F32 && scale == nullptr;
-  for (int r = warp; r < nrow; r += WARPS) {
+  auto grab_row = [&]() {
+    int v = 0;
+    if (lane == 0) v = atomicAdd(&next_row, 1);
+    return __shfl_sync(kFull, v, 0);
+  };
+  for (int r = warp; r < nrow; r = grab_row()) {
     const int64_t orow = c0 + r;
     const int i = AT.rloc[r];
     const int64_t g = a0 + i;
