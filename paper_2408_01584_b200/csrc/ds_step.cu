@@ -140,6 +140,12 @@ __device__ bool offroad_query(const ds_tables &T, const ds_config &C, int w, dou
   const float fm = 1e-3f + 2.4e-7f * (fabsf(fcx) + fabsf(fcy) + (float)(rx + ry));
   const float frx = (float)rx + fm, fry = (float)ry + fm;
   const float4 *erel = reinterpret_cast<const float4 *>(T.eseg_rel);
+  // float separating-axis filter (box axes and the segment normal) on the
+  // same copies: a separation by more than the margin (four times a bound on
+  // the float error of the box-relative endpoints and their projections)
+  // proves the exact slab test misses, so the FP64 record is not fetched
+  const float cf = (float)ck, sf = (float)sk, hlf = (float)hl, hwf = (float)hw;
+  const float e_c = 1.2e-7f * (fabsf(fcx) + fabsf(fcy)) + 1e-6f;
   const double gx0 = (cx - rx - x0) / cs, gx1 = (cx + rx - x0) / cs;
   const double gy0 = (cy - ry - y0) / cs, gy1 = (cy + ry - y0) / cs;
   if (gx1 < 0.0 || gy1 < 0.0 || gx0 >= (double)nx || gy0 >= (double)ny) return false;
@@ -160,6 +166,25 @@ __device__ bool offroad_query(const ds_tables &T, const ds_config &C, int w, dou
         if (fmaxf(q[v].x, q[v].z) < fcx - frx || fminf(q[v].x, q[v].z) > fcx + frx ||
             fmaxf(q[v].y, q[v].w) < fcy - fry || fminf(q[v].y, q[v].w) > fcy + fry)
           continue;
+        {
+          const float pax = q[v].x - fcx, pay = q[v].y - fcy, pbx = q[v].z - fcx, pby = q[v].w - fcy;
+          // |float error| of the box-relative endpoints <= e_in (input
+          // roundings of both copies and of the subtraction, long segments
+          // included); four times that plus 0.1 mm on every axis
+          const float e_in =
+              e_c + 1.2e-7f * (fabsf(pax) + fabsf(pay) + fabsf(pbx) + fabsf(pby));
+          const float mg = 4.0f * e_in + 1e-4f;
+          const float ua = pax * cf + pay * sf, ub = pbx * cf + pby * sf;
+          if (fminf(ua, ub) > hlf + mg || fmaxf(ua, ub) < -hlf - mg) continue;
+          const float va = pay * cf - pax * sf, vb = pby * cf - pbx * sf;
+          if (fminf(va, vb) > hwf + mg || fmaxf(va, vb) < -hwf - mg) continue;
+          const float nxs = pay - pby, nys = pbx - pax;   // segment normal (unnormalised)
+          const float dn = fabsf(pax * nxs + pay * nys);
+          const float rn = hlf * fabsf(cf * nxs + sf * nys) + hwf * fabsf(cf * nys - sf * nxs);
+          const float mn = mg * (fabsf(nxs) + fabsf(nys)) +
+                           8.0f * e_in * (fabsf(pax) + fabsf(pay) + hlf + hwf);
+          if (dn > rn + mn) continue;
+        }
         // FP64 endpoints: one 32-B record (one sector) per entry
         const double2 *er = reinterpret_cast<const double2 *>(T.eseg_rec) + 2 * (int64_t)(k0 + v);
         const double2 e0 = er[0], e1 = er[1];
