@@ -47,7 +47,9 @@ constexpr int kCandGlobal = 640;  // buffered pass-1 candidates (global-points v
 constexpr int kCandShared = 224;  // (shared-points variant: hint-narrowed scans)
 // warps per world CTA: as many as the shared memory allows (occupancy is what
 // hides this kernel's latencies: 16 / 24 / 28 / 32 warps measured 2.82 /
-// 2.53 / 2.28 / 2.16 ms at C3); 32 fits the default caps with 10k points
+// 2.53 / 2.28 / 2.16 ms at C3 in round 1; 28 / 30 / 32 measured 1.356 /
+// 1.401 / 1.292 ms in round 2); 32 fits the default caps with 10k points.
+// DS_OBS_WARPS: A/B builds only (tools/build_variant.sh)
 #ifndef DS_OBS_WARPS
 #define DS_OBS_WARPS 32
 #endif
