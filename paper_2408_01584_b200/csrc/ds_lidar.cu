@@ -301,6 +301,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
   const int R = C.n_rays;
   const bool full_circle = C.obs_mode == DS_OBS_LIDAR || C.fov >= kTwoPi;
 
+  // float32 rows without normalisation leave by bulk (TMA) stores
+  const bool bulk_out = O.dtype == DS_OBS_F32 && scale == nullptr;
   for (int r = warp; r < nrow; r += WARPS) {
     const int64_t orow = c0 + r;
     const int64_t g = T.row_agent[orow];
@@ -313,6 +315,11 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
     LIDAR_STAT(0, 1);
     float *const row = row0 + ((out_row_phase(O, orow) - row0_phase) & 3);
     const double ox = sx[i], oy = sy[i], h = St.heading[g];
+    if (bulk_out) {
+      // the previous row's bulk store must have read the staged row
+      if (lane == 0) bulk_row_wait();
+      __syncwarp();
+    }
     if (lane == 0) {
       // _fill_ego (obs:129-142)
       const double c = sc[i], s = ss[i];
@@ -354,7 +361,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
         const float d2 = cx * cx + cy * cy, lim = (float)max_range + cr + 1e-3f;
         if (d2 <= lim * lim) {
           int k_hi = R - 1;
-          const float dist = sqrtf(d2);
+          const float dist = sqrt_dn(d2);   // underestimate: wider span
           if (dist > cr + 1e-3f) {
             const float half = asin_upper(cr / dist) + 1e-4f;
             float rel = fast_atan2(cy, cx) - half - fcenter;
@@ -422,13 +429,13 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
             const float xlo = (float)ix * fcs, ylo = (float)iy * fcs;
             const float ddx = fmaxf(fmaxf(xlo - fox, fox - (xlo + fcs)), 0.0f);
             const float ddy = fmaxf(fmaxf(ylo - foy, foy - (ylo + fcs)), 0.0f);
-            const float dmin = sqrtf(ddx * ddx + ddy * ddy) - 2e-3f;
+            const float dmin = sqrt_dn(ddx * ddx + ddy * ddy) - 2e-3f;
             bool keep = dmin <= freach;
             if (keep && ring >= 2) {
               // bounding-circle angular span of the cell (ring >= 2: the
               // origin is at least 1.5 cells from the cell centre)
               const float ccx = xlo + 0.5f * fcs - fox, ccy = ylo + 0.5f * fcs - foy;
-              const float dc = sqrtf(ccx * ccx + ccy * ccy);
+              const float dc = sqrt_dn(ccx * ccx + ccy * ccy);
               const float half = asin_upper(cell_rad / dc) + 1e-4f;
               float rel = fast_atan2(ccy, ccx) - half - fcenter;
               rel -= (float)kTwoPi * floorf(rel * (float)kInvTwoPi);
@@ -507,7 +514,11 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
         }
         // the remaining cells lie in rings >= ring_of(q0 + 32), at least
         // (that ring - 1) cells from the origin's cell
-        const int rrem = q0 + 32 < n_cells ? ring_of(q0 + 32) : 0;   // warp-uniform
+        int rrem = 0;   // warp-uniform
+        if (q0 + 32 < n_cells) {
+          int ddx_, ddy_;
+          ring_cell(q0 + 32, table, ddx_, ddy_, rrem);
+        }
         if (rrem >= 2) {
           // float compare against far rounded down: only ever keeps walking
           // longer than the FP64 test would (extra cells cannot change hits)
@@ -544,9 +555,14 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
       slot[4] = type == 3 ? 1.0f : 0.0f;
     }
     __syncwarp();
-    write_row(O, orow, row, obs_width, scale, lane);
-    __syncwarp();
+    if (bulk_out) {
+      write_row_bulk(O, orow, row, obs_width, lane);
+    } else {
+      write_row(O, orow, row, obs_width, scale, lane);
+      __syncwarp();
+    }
   }
+  if (bulk_out && lane == 0) bulk_row_wait();   // the staging must outlive the copies
 }
 
 }  // namespace

@@ -14,6 +14,13 @@ __device__ __forceinline__ int clampf(float f, int lo, int hi) {
   return (int)fminf(fmaxf(f, (float)lo), (float)hi);
 }
 
+// A lower bound of sqrt(x) for x >= 0 from the hardware reciprocal square
+// root (relative error < 2^-21, covered by the 4e-6 factor): for culling
+// distances that may only be underestimated
+__device__ __forceinline__ float sqrt_dn(float x) {
+  return x * rsqrtf(fmaxf(x, 1e-30f)) * (1.0f - 4e-6f);
+}
+
 // Cell rows of a query disc around (px, py) -- float coordinates relative to
 // the grid origin: lane l owns row iy0 + l; the covered cells of a row are
 // one contiguous range of the cell-sorted points.  The float arithmetic is
