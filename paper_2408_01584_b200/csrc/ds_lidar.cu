@@ -348,18 +348,36 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
     __syncwarp();
     // boxes, box-major: the reference's candidates (visible, not ego, within
     // max_range + circumradius), each tested exactly only against the rays
-    // of a conservative angular interval around its bounding circle; the
-    // (box, ray) pairs of 32 boxes are flattened into full warp batches
-    for (int j0 = 0; j0 < A; j0 += 32) {
-      const int j = j0 + lane;
-      int k_lo = 0, n_k = 0;
-      if (j < A && j != i && svis[j]) {
-        // float superset of the candidates: a box whose centre is farther
-        // than max_range + circumradius cannot be hit within max_range
-        const float cx = (float)(sx[j] - ox), cy = (float)(sy[j] - oy);
-        const float cr = (float)scr[j] + 1e-3f;
-        const float d2 = cx * cx + cy * cy, lim = (float)max_range + cr + 1e-3f;
-        if (d2 <= lim * lim) {
+    // of a conservative angular interval around its bounding circle.  The
+    // candidates of up to 256 agents are first compacted (into the idle
+    // segment cache), then their (box, ray) pairs are flattened into full
+    // warp batches
+    int *const clist = reinterpret_cast<int *>(seg_ax);
+    for (int a0c = 0; a0c < A; a0c += 256) {
+      int ncand = 0;
+      for (int j0 = a0c; j0 < min(A, a0c + 256); j0 += 32) {
+        const int j = j0 + lane;
+        bool cand = false;
+        if (j < A && j != i && svis[j]) {
+          // float superset of the candidates: a box whose centre is farther
+          // than max_range + circumradius cannot be hit within max_range
+          const float cx = (float)(sx[j] - ox), cy = (float)(sy[j] - oy);
+          const float cr = (float)scr[j] + 1e-3f;
+          const float lim = (float)max_range + cr + 1e-3f;
+          cand = cx * cx + cy * cy <= lim * lim;
+        }
+        const unsigned bal = __ballot_sync(kFullMask, cand);
+        if (cand) clist[ncand + __popc(bal & ((1u << lane) - 1u))] = j;
+        ncand += __popc(bal);
+      }
+      __syncwarp();
+      for (int c0 = 0; c0 < ncand; c0 += 32) {
+        int k_lo = 0, n_k = 0;
+        if (c0 + lane < ncand) {
+          const int j = clist[c0 + lane];
+          const float cx = (float)(sx[j] - ox), cy = (float)(sy[j] - oy);
+          const float cr = (float)scr[j] + 1e-3f;
+          const float d2 = cx * cx + cy * cy;
           int k_hi = R - 1;
           const float dist = sqrt_dn(d2);   // underestimate: wider span
           if (dist > cr + 1e-3f) {
@@ -370,22 +388,23 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
           }
           n_k = k_hi - k_lo + 1 > 0 ? k_hi - k_lo + 1 : 0;
         }
-      }
-      FlatRows pairs;
-      pairs.build(k_lo, n_k, lane, fscr);
-      LIDAR_STAT(1, pairs.total);          // exact ray-box slab tests
-      for (int p0 = 0; p0 < pairs.total; p0 += 32) {
-        int owner;
-        const int m = pairs.map_owner(p0, lane, owner);
-        const int jj = j0 + owner;
-        if (p0 + lane < pairs.total) {
-          const int k = m >= R ? m - R : m;
-          const double d = ray_box(ox, oy, rdx[k], rdy[k], sx[jj], sy[jj], sc[jj], ss[jj], shl[jj],
-                                   shw[jj]);
-          if (d != INFINITY)   // d >= 0; + 0.0 maps -0 to +0 so the bit order is the value order
-            atomicMin(&rbest[k], (unsigned long long)__double_as_longlong(d + 0.0));
+        FlatRows pairs;
+        pairs.build(k_lo, n_k, lane, fscr);
+        LIDAR_STAT(1, pairs.total);          // exact ray-box slab tests
+        for (int p0 = 0; p0 < pairs.total; p0 += 32) {
+          int owner;
+          const int m = pairs.map_owner(p0, lane, owner);
+          if (p0 + lane < pairs.total) {
+            const int jj = clist[c0 + owner];
+            const int k = m >= R ? m - R : m;
+            const double d = ray_box(ox, oy, rdx[k], rdy[k], sx[jj], sy[jj], sc[jj], ss[jj], shl[jj],
+                                     shw[jj]);
+            if (d != INFINITY)   // d >= 0; + 0.0 maps -0 to +0 so the bit order is the value order
+              atomicMin(&rbest[k], (unsigned long long)__double_as_longlong(d + 0.0));
+          }
         }
       }
+      __syncwarp();
     }
     __syncwarp();
     // per-ray limit for the segment phase: the box hit or max_range
