@@ -25,6 +25,7 @@ import ctypes as C
 import math
 import time
 import warnings
+from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -147,6 +148,31 @@ def default_grid_cell(obs: ObsConfig) -> float:
     return 10.0
 
 
+class AgentIndex(Sequence):
+    """SimBatch.agent_index (engine.py:609): the (world, agent) pair of every
+    controlled row, in row order -- a lazy, read-only sequence over the packed
+    row table (equal to the reference's list of tuples, without building
+    n_rows Python tuples for 4096-world batches)."""
+
+    def __init__(self, pw):
+        self._world = np.repeat(np.arange(pw.n_worlds, dtype=np.int64), np.diff(pw.c_off))
+        self._agent = pw.row_agent.astype(np.int64) - pw.a_off[self._world]
+
+    def __len__(self) -> int:
+        return len(self._world)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        return (int(self._world[i]), int(self._agent[i]))
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+    def __repr__(self) -> str:
+        return f"AgentIndex({len(self)} rows)"
+
+
 class _WorldView:
     """Read-only snapshot view of one world (the attributes tests read from
     reference World objects: t, controlled_ids, replay tables, dt ...)."""
@@ -251,8 +277,7 @@ class SimBatch:
         for w in np.nonzero(np.diff(pw.c_off) == 0)[0]:
             warnings.warn(f"world {w} ({pw.names[w]}): no controllable agents, replay-only",
                           NoControllableAgents)
-        self.agent_index = [(int(w), int(a)) for w in range(self.n_worlds)
-                            for a in pw.controlled_ids(w)] if self.n_controlled < 200_000 else None
+        self.agent_index = AgentIndex(pw)
         self.grid_cell = grid_cell or default_grid_cell(cfg.obs)
         if cfg.obs.mode == "radial":
             self.grid_cell = max(self.grid_cell, (2.0 * cfg.obs.radius + 2.0) / 30.0)
