@@ -45,9 +45,10 @@ constexpr int kLidarWarps = 16;
 
 __host__ __device__ inline size_t al16l(size_t v) { return (v + 15) & ~size_t(15); }
 
-// per-agent shared arrays: x, y, c, s, hl, hw, circumradius (f64) + vis (u8)
+// per-agent shared arrays: x, y, c, s, hl, hw, circumradius (f64) + vis (u8),
+// then the ego block of every agent (7 floats, padded to 8)
 __host__ __device__ inline size_t lidar_agents_bytes(int amax) {
-  return al16l((size_t)amax * (7 * sizeof(double) + 1));
+  return al16l((size_t)amax * (7 * sizeof(double) + 1)) + (size_t)amax * 8 * sizeof(float);
 }
 
 // per warp: ray dx, dy, box-min bits, segment-key min, limit (8 B each), the
@@ -281,16 +282,31 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
 
   const int64_t a0 = T.a_off[w];
   const int A = (int)(T.a_off[w + 1] - a0);
+  float *sego = reinterpret_cast<float *>(smem_raw + al16l((size_t)amax * (7 * sizeof(double) + 1)));
   for (int i = threadIdx.x; i < A; i += blockDim.x) {
     const int64_t g = a0 + i;
-    sx[i] = St.x[g];
-    sy[i] = St.y[g];
-    sincos(St.heading[g], &ss[i], &sc[i]);
+    const double x = St.x[g], y = St.y[g];
+    double c, s;
+    sincos(St.heading[g], &s, &c);
+    sx[i] = x;
+    sy[i] = y;
+    sc[i] = c;
+    ss[i] = s;
     shl[i] = T.half_l[g];
     shw[i] = T.half_w[g];
     scr[i] = T.circumradius[g];
     const uint16_t f = St.flags[g];
     svis[i] = (f & DS_F_PRESENT) && !(f & DS_F_REMOVED);
+    // _fill_ego (obs:129-142), once per agent instead of per row on one lane
+    const double gx = T.goal_x[g] - x, gy = T.goal_y[g] - y;
+    float *e = sego + 8 * i;
+    e[0] = (float)St.speed[g];
+    e[1] = (float)T.length[g];
+    e[2] = (float)T.width[g];
+    e[3] = (float)(gx * c + gy * s);
+    e[4] = (float)(-gx * s + gy * c);
+    e[5] = (float)hypot(gx, gy);
+    e[6] = (f & DS_F_COLLIDED) ? 1.0f : 0.0f;
   }
   __syncthreads();
 
@@ -320,18 +336,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
       if (lane == 0) bulk_row_wait();
       __syncwarp();
     }
-    if (lane == 0) {
-      // _fill_ego (obs:129-142)
-      const double c = sc[i], s = ss[i];
-      const double gx = T.goal_x[g] - ox, gy = T.goal_y[g] - oy;
-      row[0] = (float)St.speed[g];
-      row[1] = (float)T.length[g];
-      row[2] = (float)T.width[g];
-      row[3] = (float)(gx * c + gy * s);
-      row[4] = (float)(-gx * s + gy * c);
-      row[5] = (float)hypot(gx, gy);
-      row[6] = (f & DS_F_COLLIDED) ? 1.0f : 0.0f;
-    }
+    if (lane < 7) row[lane] = sego[8 * i + lane];   // ego block, formed in the prologue
     double center = h;
     if (C.obs_mode == DS_OBS_VIEW_CONE) center += St.head_angle[g];
     const float fcenter = (float)center;
