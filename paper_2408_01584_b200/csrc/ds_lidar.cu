@@ -254,6 +254,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
   const int nrow = (int)(T.c_off[w + 1] - c0);
   if (nrow == 0) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int next_row;
+  if (threadIdx.x == 0) next_row = WARPS;
   const int amax = T.max_agents;
   double *sx = reinterpret_cast<double *>(smem_raw);
   double *sy = sx + amax, *sc = sx + 2 * amax, *ss = sx + 3 * amax, *shl = sx + 4 * amax,
@@ -319,7 +321,14 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
 
   // float32 rows without normalisation leave by bulk (TMA) stores
   const bool bulk_out = O.dtype == DS_OBS_F32 && scale == nullptr;
-  for (int r = warp; r < nrow; r += WARPS) {
+  // rows are handed out dynamically after a static first row per warp
+  // (a row's cost varies with how far its rays reach)
+  auto grab_row = [&]() {
+    int v = 0;
+    if (lane == 0) v = atomicAdd(&next_row, 1);
+    return __shfl_sync(kFullMask, v, 0);
+  };
+  for (int r = warp; r < nrow; r = grab_row()) {
     const int64_t orow = c0 + r;
     const int64_t g = T.row_agent[orow];
     const int i = (int)(g - a0);
@@ -599,8 +608,13 @@ size_t lidar_smem_bytes(int max_agents, int obs_width) {
 int lidar_warps() { return kLidarWarps; }
 
 cudaError_t configure_lidar_kernels(int max_dynamic_smem) {
+  // the opt-in limit covers static + dynamic shared memory (the row counter)
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, obs_lidar_kernel<kLidarWarps>);
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(obs_lidar_kernel<kLidarWarps>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, max_dynamic_smem);
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              max_dynamic_smem - (int)fa.sharedSizeBytes);
 }
 
 cudaError_t launch_lidar(const ds_handle *h, const uint8_t *mask, void *obs, const float *scale,
