@@ -41,7 +41,12 @@ __device__ unsigned long long g_lidar_stats[8];
 
 namespace {
 
-constexpr int kLidarWarps = 16;
+// warps per world CTA (2 CTAs per SM): 8 / 12 / 16 / 32 measured 4.94 /
+// 5.28 / 4.82 / 5.12 ms at C4 (round 2).  DS_LIDAR_WARPS: A/B builds only
+#ifndef DS_LIDAR_WARPS
+#define DS_LIDAR_WARPS 16
+#endif
+constexpr int kLidarWarps = DS_LIDAR_WARPS;
 
 __host__ __device__ inline size_t al16l(size_t v) { return (v + 15) & ~size_t(15); }
 
