@@ -249,10 +249,14 @@ __device__ __forceinline__ double ray_box(double ox, double oy, double dx, doubl
   return ok ? fmax(tmin, 0.0) : INFINITY;
 }
 
-template <int WARPS>
+// NR > 0: the ray count as a compile-time constant (the default 64: every
+// per-warp array sits at a constant offset and the per-ray loops unroll);
+// 0: taken from the config at run time
+template <int WARPS, int NR>
 __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 : 1)) obs_lidar_kernel(
     ds_tables T, ds_config C, ds_state St, const uint8_t *mask, const ObsOut O, const float *scale,
     int obs_width) {
+  const int R = NR > 0 ? NR : C.n_rays;
   const int w = blockIdx.x;
   if (mask && !mask[w]) return;
   const int64_t c0 = T.c_off[w];
@@ -267,14 +271,14 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
          *shw = sx + 5 * amax, *scr = sx + 6 * amax;
   uint8_t *svis = reinterpret_cast<uint8_t *>(sx + 7 * amax);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t per_warp = lidar_warp_bytes(obs_width, C.n_rays);
+  const size_t per_warp = NR > 0 ? lidar_warp_bytes(7 + 5 * NR, NR) : lidar_warp_bytes(obs_width, R);
   unsigned char *wb = smem_raw + lidar_agents_bytes(amax) + (size_t)warp * per_warp;
   double *rdx = reinterpret_cast<double *>(wb);
-  double *rdy = rdx + C.n_rays;
-  double *rlim = rdy + C.n_rays;
-  unsigned long long *rbest = reinterpret_cast<unsigned long long *>(rlim + C.n_rays);
-  unsigned long long *rseg = rbest + C.n_rays;
-  double *seg_ax = reinterpret_cast<double *>(rseg + C.n_rays);
+  double *rdy = rdx + R;
+  double *rlim = rdy + R;
+  unsigned long long *rbest = reinterpret_cast<unsigned long long *>(rlim + R);
+  unsigned long long *rseg = rbest + R;
+  double *seg_ax = reinterpret_cast<double *>(rseg + R);
   double *seg_ay = seg_ax + 32, *seg_bx = seg_ax + 64, *seg_by = seg_ax + 96;
   uint8_t *seg_ne = reinterpret_cast<uint8_t *>(seg_ax + 128);
   // per-ray float upper bound of the road search bound (limit / best segment
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
   float *rbf = reinterpret_cast<float *>(fscr + 32);
   float *const row0 = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(seg_ax) +
                                                 al16l(kSegCacheBytes) + 32 * sizeof(int) +
-                                                al16l((size_t)C.n_rays * sizeof(float)));
+                                                al16l((size_t)R * sizeof(float)));
   const int row0_phase = (int)((reinterpret_cast<uintptr_t>(row0) >> 2) & 3);
 
   const int64_t a0 = T.a_off[w];
@@ -321,7 +325,6 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
   const double gx0 = T.grid_x0[w], gy0 = T.grid_y0[w], cs = C.grid_cell;
   const int gnx = T.grid_nx[w], gny = T.grid_ny[w];
   const double max_range = C.max_range;
-  const int R = C.n_rays;
   const bool full_circle = C.obs_mode == DS_OBS_LIDAR || C.fov >= kTwoPi;
 
   // float32 rows without normalisation leave by bulk (TMA) stores
@@ -614,19 +617,28 @@ int lidar_warps() { return kLidarWarps; }
 
 cudaError_t configure_lidar_kernels(int max_dynamic_smem) {
   // the opt-in limit covers static + dynamic shared memory (the row counter)
-  cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, obs_lidar_kernel<kLidarWarps>);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(obs_lidar_kernel<kLidarWarps>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              max_dynamic_smem - (int)fa.sharedSizeBytes);
+  const void *ks[] = {(const void *)obs_lidar_kernel<kLidarWarps, 64>,
+                      (const void *)obs_lidar_kernel<kLidarWarps, 0>};
+  for (const void *k : ks) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             max_dynamic_smem - (int)fa.sharedSizeBytes);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_lidar(const ds_handle *h, const uint8_t *mask, void *obs, const float *scale,
                          cudaStream_t s) {
   const ObsOut O{obs, h->obs_dtype, h->obs_stride};
-  obs_lidar_kernel<kLidarWarps><<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(
-      h->tab, h->cfg, h->st, mask, O, scale, h->obs_width);
+  if (h->cfg.n_rays == 64)
+    obs_lidar_kernel<kLidarWarps, 64><<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(
+        h->tab, h->cfg, h->st, mask, O, scale, h->obs_width);
+  else
+    obs_lidar_kernel<kLidarWarps, 0><<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(
+        h->tab, h->cfg, h->st, mask, O, scale, h->obs_width);
   return cudaGetLastError();
 }
 
