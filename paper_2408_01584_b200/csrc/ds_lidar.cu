@@ -251,8 +251,9 @@ __device__ __forceinline__ double ray_box(double ox, double oy, double dx, doubl
 
 // NR > 0: the ray count as a compile-time constant (the default 64: every
 // per-warp array sits at a constant offset and the per-ray loops unroll);
-// 0: taken from the config at run time
-template <int WARPS, int NR>
+// 0: taken from the config at run time.  FULL: a full-circle sweep known at
+// compile time (LiDAR), else decided from the config (view cone)
+template <int WARPS, int NR, bool FULL>
 __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 : 1)) obs_lidar_kernel(
     ds_tables T, ds_config C, ds_state St, const uint8_t *mask, const ObsOut O, const float *scale,
     int obs_width) {
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
   const double gx0 = T.grid_x0[w], gy0 = T.grid_y0[w], cs = C.grid_cell;
   const int gnx = T.grid_nx[w], gny = T.grid_ny[w];
   const double max_range = C.max_range;
-  const bool full_circle = C.obs_mode == DS_OBS_LIDAR || C.fov >= kTwoPi;
+  const bool full_circle = FULL || C.obs_mode == DS_OBS_LIDAR || C.fov >= kTwoPi;
 
   // float32 rows without normalisation leave by bulk (TMA) stores
   const bool bulk_out = O.dtype == DS_OBS_F32 && scale == nullptr;
@@ -617,8 +618,8 @@ int lidar_warps() { return kLidarWarps; }
 
 cudaError_t configure_lidar_kernels(int max_dynamic_smem) {
   // the opt-in limit covers static + dynamic shared memory (the row counter)
-  const void *ks[] = {(const void *)obs_lidar_kernel<kLidarWarps, 64>,
-                      (const void *)obs_lidar_kernel<kLidarWarps, 0>};
+  const void *ks[] = {(const void *)obs_lidar_kernel<kLidarWarps, 64, true>,
+                      (const void *)obs_lidar_kernel<kLidarWarps, 0, false>};
   for (const void *k : ks) {
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, k);
@@ -633,11 +634,12 @@ cudaError_t configure_lidar_kernels(int max_dynamic_smem) {
 cudaError_t launch_lidar(const ds_handle *h, const uint8_t *mask, void *obs, const float *scale,
                          cudaStream_t s) {
   const ObsOut O{obs, h->obs_dtype, h->obs_stride};
-  if (h->cfg.n_rays == 64)
-    obs_lidar_kernel<kLidarWarps, 64><<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(
+  const bool full = h->cfg.obs_mode == DS_OBS_LIDAR || h->cfg.fov >= kTwoPi;
+  if (h->cfg.n_rays == 64 && full)
+    obs_lidar_kernel<kLidarWarps, 64, true><<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(
         h->tab, h->cfg, h->st, mask, O, scale, h->obs_width);
   else
-    obs_lidar_kernel<kLidarWarps, 0><<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(
+    obs_lidar_kernel<kLidarWarps, 0, false><<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(
         h->tab, h->cfg, h->st, mask, O, scale, h->obs_width);
   return cudaGetLastError();
 }
