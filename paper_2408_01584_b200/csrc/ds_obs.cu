@@ -61,6 +61,7 @@ constexpr int kWarpsSharedSmall = 24;
 constexpr int kWarpsSharedPair = 16;
 constexpr int kSmemPerSM = 228 * 1024;
 constexpr int kWarpsGlobal = 12;
+constexpr int kAgentStride = 128;   // compile-time agent-table stride (AMAX)
 // static shared memory of the radial kernel (mbarrier, per-warp rounding
 // maxima, row counter): an upper bound for the launch plan
 constexpr size_t kStaticSmem = 256;
@@ -880,7 +881,10 @@ struct RadialK {
   double radius, reach, r2, D_fp64, cs, inv_cs, key_e;
 };
 
-template <int WARPS, bool SharedPts, int CAPA, int CAPR>
+// AMAX > 0: the agent tables' stride as a compile-time constant (worlds of
+// <= AMAX agents; every agent array then sits at a constant offset from one
+// base instead of a dozen run-time pointers); 0: T.max_agents
+template <int WARPS, bool SharedPts, int CAPA, int CAPR, int AMAX = 0>
 __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 1) obs_radial_kernel(
     ds_tables T, ds_config C, ds_state St, const RadialK K, const uint8_t *mask, const ObsOut O,
     const float *scale, int32_t *sel_idx, int obs_width) {
@@ -921,7 +925,7 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   unsigned char *const sbase = static_cast<unsigned char *>(__cvta_shared_to_generic(smem_s));
   unsigned char *wb = sbase + WL.total * warp;
   unsigned char *after_scratch = sbase + WL.total * WARPS;
-  const int amax = T.max_agents;
+  const int amax = AMAX > 0 ? AMAX : T.max_agents;
   // points: the 16-B aligned body [pa, pb) of the world's range by one bulk
   // copy, an odd head / tail point by plain loads; pts[j] = point p0 + j
   float2 *const pbuf = reinterpret_cast<float2 *>(after_scratch);
@@ -1239,7 +1243,10 @@ namespace ds {
 #endif
 
 cudaError_t configure_kernels(int max_dynamic_smem) {
-  const void *ks[] = {(const void *)obs_radial_kernel<kWarpsShared, true, 16, 64>,
+  const void *ks[] = {(const void *)obs_radial_kernel<kWarpsShared, true, 16, 64, kAgentStride>,
+                      (const void *)obs_radial_kernel<kWarpsSharedSmall, true, 16, 64, kAgentStride>,
+                      (const void *)obs_radial_kernel<kWarpsSharedPair, true, 16, 64, kAgentStride>,
+                      (const void *)obs_radial_kernel<kWarpsShared, true, 16, 64>,
                       (const void *)obs_radial_kernel<kWarpsShared, true, 0, 0>,
                       (const void *)obs_radial_kernel<kWarpsSharedSmall, true, 16, 64>,
                       (const void *)obs_radial_kernel<kWarpsSharedSmall, true, 0, 0>,
@@ -1262,6 +1269,16 @@ cudaError_t configure_kernels(int max_dynamic_smem) {
   return configure_step_kernels(max_dynamic_smem);
 }
 
+static bool obs_fixed_caps(const ds_handle *h) {
+  return h->cfg.max_agents_obs == 16 && h->cfg.max_road_points_obs == 64;
+}
+
+// the agent-table stride of the shared-points kernels: kAgentStride when the
+// fixed-cap variant runs on worlds of <= kAgentStride agents
+static int obs_agent_stride(const ds_handle *h) {
+  return obs_fixed_caps(h) && h->tab.max_agents <= kAgentStride ? kAgentStride : h->tab.max_agents;
+}
+
 void obs_plan(ds_handle *h, int max_optin) {
   if (h->cfg.obs_mode != DS_OBS_RADIAL) {
     h->obs_shared_pts = 0;
@@ -1270,11 +1287,10 @@ void obs_plan(ds_handle *h, int max_optin) {
     return;
   }
   const bool can = h->tab.gpt_xy && h->tab.grid_eps && h->tab.gpt_rec;
-  const size_t sh = obs_smem_bytes_shared(h->cfg, h->tab.max_agents, h->tab.max_points, kWarpsShared);
-  const size_t sh_small =
-      obs_smem_bytes_shared(h->cfg, h->tab.max_agents, h->tab.max_points, kWarpsSharedSmall);
-  const size_t sh_pair =
-      obs_smem_bytes_shared(h->cfg, h->tab.max_agents, h->tab.max_points, kWarpsSharedPair);
+  const int am = obs_agent_stride(h);
+  const size_t sh = obs_smem_bytes_shared(h->cfg, am, h->tab.max_points, kWarpsShared);
+  const size_t sh_small = obs_smem_bytes_shared(h->cfg, am, h->tab.max_points, kWarpsSharedSmall);
+  const size_t sh_pair = obs_smem_bytes_shared(h->cfg, am, h->tab.max_points, kWarpsSharedPair);
   if (can && h->tab.max_agents <= 64 && h->tab.n_worlds >= 2 * h->num_sms &&
       2 * (sh_pair + 1024) <= (size_t)kSmemPerSM) {
     h->obs_shared_pts = 1;
@@ -1310,7 +1326,10 @@ struct ObsLaunch {
 template <int WARPS, bool SharedPts>
 void launch_radial(const ObsLaunch &L) {
   const ds_handle *h = L.h;
-  if (L.fixed)
+  if (SharedPts && L.fixed && obs_agent_stride(h) == kAgentStride)
+    obs_radial_kernel<WARPS, SharedPts, 16, 64, kAgentStride><<<L.W, WARPS * 32, h->obs_smem, L.s>>>(
+        h->tab, h->cfg, h->st, L.K, L.mask, L.O, L.scale, L.sel_idx, h->obs_width);
+  else if (L.fixed)
     obs_radial_kernel<WARPS, SharedPts, 16, 64><<<L.W, WARPS * 32, h->obs_smem, L.s>>>(
         h->tab, h->cfg, h->st, L.K, L.mask, L.O, L.scale, L.sel_idx, h->obs_width);
   else
