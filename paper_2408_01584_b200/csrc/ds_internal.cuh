@@ -34,7 +34,7 @@ cudaError_t launch_reset(const ds_handle *h, const uint8_t *mask, float *rewards
 cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, void *obs,
                            const float *scale, int32_t *sel_idx, cudaStream_t s);
 void obs_plan(ds_handle *h, int max_dynamic_smem);
-size_t lidar_smem_bytes(int max_agents, int obs_width);
+size_t lidar_smem_bytes(const ds_config &cfg, int max_agents, int obs_width);
 int lidar_warps();
 cudaError_t configure_lidar_kernels(int max_dynamic_smem);
 cudaError_t launch_lidar(const ds_handle *h, const uint8_t *mask, void *obs, const float *scale,

@@ -252,8 +252,10 @@ __device__ __forceinline__ double ray_box(double ox, double oy, double dx, doubl
 // NR > 0: the ray count as a compile-time constant (the default 64: every
 // per-warp array sits at a constant offset and the per-ray loops unroll);
 // 0: taken from the config at run time.  FULL: a full-circle sweep known at
-// compile time (LiDAR), else decided from the config (view cone)
-template <int WARPS, int NR, bool FULL>
+// compile time (LiDAR), else decided from the config (view cone).  AMAX > 0:
+// the agent tables' stride as a compile-time constant (worlds of <= AMAX
+// agents), 0: T.max_agents
+template <int WARPS, int NR, bool FULL, int AMAX>
 __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 : 1)) obs_lidar_kernel(
     ds_tables T, ds_config C, ds_state St, const uint8_t *mask, const ObsOut O, const float *scale,
     int obs_width) {
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int next_row;
   if (threadIdx.x == 0) next_row = WARPS;
-  const int amax = T.max_agents;
+  const int amax = AMAX > 0 ? AMAX : T.max_agents;
   double *sx = reinterpret_cast<double *>(smem_raw);
   double *sy = sx + amax, *sc = sx + 2 * amax, *ss = sx + 3 * amax, *shl = sx + 4 * amax,
          *shw = sx + 5 * amax, *scr = sx + 6 * amax;
@@ -609,17 +611,25 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
 
 }  // namespace
 
-size_t lidar_smem_bytes(int max_agents, int obs_width) {
+// the fast variant: 64 rays over the full circle, worlds of <= 128 agents
+// (agent tables at the compile-time stride 128)
+constexpr int kLidarStride = 128;
+static bool lidar_fast(const ds_config &c, int max_agents) {
+  return c.n_rays == 64 && (c.obs_mode == DS_OBS_LIDAR || c.fov >= kTwoPi) && max_agents <= kLidarStride;
+}
+
+size_t lidar_smem_bytes(const ds_config &cfg, int max_agents, int obs_width) {
   const int n_rays = (obs_width - 7) / 5;
-  return lidar_agents_bytes(max_agents) + (size_t)kLidarWarps * lidar_warp_bytes(obs_width, n_rays);
+  const int am = lidar_fast(cfg, max_agents) ? kLidarStride : max_agents;
+  return lidar_agents_bytes(am) + (size_t)kLidarWarps * lidar_warp_bytes(obs_width, n_rays);
 }
 
 int lidar_warps() { return kLidarWarps; }
 
 cudaError_t configure_lidar_kernels(int max_dynamic_smem) {
   // the opt-in limit covers static + dynamic shared memory (the row counter)
-  const void *ks[] = {(const void *)obs_lidar_kernel<kLidarWarps, 64, true>,
-                      (const void *)obs_lidar_kernel<kLidarWarps, 0, false>};
+  const void *ks[] = {(const void *)obs_lidar_kernel<kLidarWarps, 64, true, kLidarStride>,
+                      (const void *)obs_lidar_kernel<kLidarWarps, 0, false, 0>};
   for (const void *k : ks) {
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, k);
@@ -634,12 +644,12 @@ cudaError_t configure_lidar_kernels(int max_dynamic_smem) {
 cudaError_t launch_lidar(const ds_handle *h, const uint8_t *mask, void *obs, const float *scale,
                          cudaStream_t s) {
   const ObsOut O{obs, h->obs_dtype, h->obs_stride};
-  const bool full = h->cfg.obs_mode == DS_OBS_LIDAR || h->cfg.fov >= kTwoPi;
-  if (h->cfg.n_rays == 64 && full)
-    obs_lidar_kernel<kLidarWarps, 64, true><<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(
-        h->tab, h->cfg, h->st, mask, O, scale, h->obs_width);
+  if (lidar_fast(h->cfg, h->tab.max_agents))
+    obs_lidar_kernel<kLidarWarps, 64, true, kLidarStride>
+        <<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(h->tab, h->cfg, h->st, mask, O,
+                                                                 scale, h->obs_width);
   else
-    obs_lidar_kernel<kLidarWarps, 0, false><<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(
+    obs_lidar_kernel<kLidarWarps, 0, false, 0><<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(
         h->tab, h->cfg, h->st, mask, O, scale, h->obs_width);
   return cudaGetLastError();
 }

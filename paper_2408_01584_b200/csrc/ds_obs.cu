@@ -1283,7 +1283,7 @@ void obs_plan(ds_handle *h, int max_optin) {
   if (h->cfg.obs_mode != DS_OBS_RADIAL) {
     h->obs_shared_pts = 0;
     h->obs_warps = lidar_warps();
-    h->obs_smem = lidar_smem_bytes(h->tab.max_agents, h->obs_width);
+    h->obs_smem = lidar_smem_bytes(h->cfg, h->tab.max_agents, h->obs_width);
     return;
   }
   const bool can = h->tab.gpt_xy && h->tab.grid_eps && h->tab.gpt_rec;
