@@ -17,6 +17,7 @@
 namespace ds {
 
 constexpr int kStepBins = 64;   // x-bins of the agent-agent sweep
+constexpr int kStepStride = 128;   // table stride of the <= 128-agent variant
 
 struct StepShared {
   double *x, *y, *c, *s, *hl, *hw, *cr;
@@ -60,6 +61,7 @@ __device__ __forceinline__ StepShared carve_step(void *base, int amax) {
 }
 
 size_t step_smem_bytes(int max_agents) {
+  if (max_agents <= kStepStride) max_agents = kStepStride;   // the <= 128-agent variant's stride
   return (size_t)max_agents * (7 * sizeof(double) + 2) + 16 + (size_t)max_agents * sizeof(float4) +
          (size_t)pow2_at_least(max_agents) * (sizeof(float) + sizeof(int)) +
          (2 * kStepBins + 1) * sizeof(int);
@@ -252,7 +254,9 @@ __global__ void __launch_bounds__(MAXT, MINB) step_kernel(ds_tables T, ds_config
     return;
   }
 
-  StepShared sh = carve_step(smem_raw, T.max_agents);
+  // the <= 128-agent variant lays its tables out at the compile-time stride
+  // 128 (every array at a constant offset; step_smem_bytes sizes it so)
+  StepShared sh = carve_step(smem_raw, MAXT <= kStepStride ? kStepStride : T.max_agents);
   const int t = S.t[w];
   const int t_next = min(t + 1, Tw - 1);
   const double dt = T.dt[w];
