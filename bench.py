@@ -536,7 +536,9 @@ def time_leg(leg: Leg, args, world: int, barrier, local_rank: int) -> dict:
             rew = leg.step(t)
             rsum_h.copy_(rew.sum().reshape(1), non_blocking=True)
         else:
-            stepper.step(host_acts[t % 8])
+            # the actions already live in pinned host buffers (8, reused every
+            # 8 steps, long after their DMA): copied straight from them
+            stepper.step(host_acts[t % 8], zero_copy=True)
 
     leg.restart()
     for t in range(args.warmup):          # untimed warm-up of this leg's own ops
