@@ -94,3 +94,42 @@ def test_full_circle_view_cone_equals_lidar():
     for (o1, r1, d1, i1), (o2, r2, d2, i2) in zip(*outs):
         assert np.array_equal(o1, o2)
         assert np.array_equal(r1, r2) and np.array_equal(d1, d2) and np.array_equal(i1, i2)
+
+
+@pytest.mark.parametrize("hint", ["bogus_small", "bogus_large", "none"])
+def test_search_hint_never_changes_results(hint):
+    """The radial search hint (last step's k-th distance bound and position)
+    only narrows a provably sufficient disc: a deliberately wrong hint -- far
+    too small (the narrowed histogram's validation must reject it and rerun
+    on the full radius), far too large, or none -- gives bit-identical
+    observations and selection indices."""
+    raw = generate(WaymoSpec(n_worlds=12, n_agents=64, n_points=3000, seed=21, quantize=False))
+    cfg = SimConfig(init_mode="all_valid", dynamics="delta_local")
+    a, b = (SimBatch.from_raw(raw, cfg, device="cuda:0") for _ in range(2))
+    sel_w = cfg.obs.max_agents_obs + cfg.obs.max_road_points_obs
+    sa, sb = (torch.full((a.n_controlled, sel_w), -7, dtype=torch.int32, device="cuda:0")
+              for _ in range(2))
+    rng = np.random.default_rng(4)
+    a.reset(sel_idx=sa)
+    b.reset(sel_idx=sb)
+    for t in range(6):
+        act = torch.from_numpy(actions_for(cfg, a.n_controlled, rng)).cuda()
+        a.step(act, sel_idx=sa)
+        b.step(act, sel_idx=sb)
+        torch.cuda.synchronize()
+        assert torch.equal(a.observations, b.observations) and torch.equal(sa, sb)
+        # corrupt b's hint for its next step (columns: bound, x, y of the
+        # position it was taken at, grid-relative)
+        h = b._hint
+        if hint == "bogus_small":
+            h[:, 0] = 0.5
+        elif hint == "bogus_large":
+            h[:, 0] = 1e4
+        else:
+            h.zero_()
+        b.observe(sel_idx=sb)
+        torch.cuda.synchronize()
+        assert torch.equal(a.observations, b.observations), f"step {t}: observations differ"
+        assert torch.equal(sa, sb), f"step {t}: selections differ"
+    a.close()
+    b.close()
