@@ -218,9 +218,18 @@ __device__ __forceinline__ double ray_segment(double ox, double oy, double dx, d
   if (us > ad * (1.0 + 1e-15)) return INFINITY;
   if (ts > beat * ad * (1.0 + 1e-15)) return INFINITY;
   const double t = tn / denom;
-  const double u = un / denom;
-  if (t >= 0.0 && u >= 0.0 && u <= 1.0) return t;
-  return INFINITY;
+  // 0 <= us <= ad (1 - 1e-15) (the product rounded at most one ulp up, still
+  // below ad) proves 0 <= u = us / ad < 1, so the rounded quotient lies in
+  // [0, 1] without dividing; only u near 0- or 1 takes the reference's
+  // division
+  bool u_ok;
+  if (us >= 0.0 && us <= ad * (1.0 - 1e-15)) {
+    u_ok = true;
+  } else {
+    const double u = un / denom;
+    u_ok = u >= 0.0 && u <= 1.0;
+  }
+  return t >= 0.0 && u_ok ? t : INFINITY;
 }
 
 // raycast_obbs_arr (geo:399-424) for one ray and one box; inf = miss.
