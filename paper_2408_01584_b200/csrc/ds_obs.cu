@@ -1,30 +1,35 @@
 // ds_obs.cu -- radial observation kernel (World._fill_obs, engine.py:500-512;
 // fill_radial / radial_fill_core, observation.py:145-210, _fastpath.py:214-302).
 //
-// Layout: one CTA per world, one warp per controlled agent (rows strided over
-// the CTA's warps).  The world's agents (FP64) and -- when they fit -- the
-// world's road points (float2 coordinates relative to the world grid origin,
-// 8 B/point) are staged once in shared memory; every warp then scans them.
-// Road candidates come from the world's uniform grid: lane l owns cell row
-// iy0 + l of the radius disc, whose covered cells form ONE contiguous,
-// cell-sorted point range.
+// Layout: one CTA per world, one warp per controlled agent (rows handed to
+// warps dynamically).  The world's road points (float2 relative to the world
+// grid origin, 8 B/point) arrive in shared memory by one TMA bulk copy while
+// the threads stage the agent tables and every per-agent selection parameter;
+// each warp then scans them.  Road candidates come from the world's uniform
+// grid: lane l owns cell row iy0 + l of the search disc, whose covered cells
+// form ONE contiguous, cell-sorted point range.
 //
 // Exact top-k (the reference's insertion sort = ascending (distance, index)):
-//  pass 1  every candidate gets a cheap float key a ~ d^2 with a proven
-//          absolute error bound D; a 128-bucket histogram of a over
-//          [0, r^2 + D] gives the threshold bucket b* (first bucket whose
-//          cumulative count reaches k);
-//  pass 2  candidates in buckets <= b*+1 are counting-sort scattered into a
-//          small set G (about k+1 entries);
-//  exact   only G gets the glibc-exact FP64 hypot (ds_math.cuh), the exact
-//          radius test and an exact (d, id) rank.  Since |a - d^2| <= D, key
-//          order inversions only involve ADJACENT buckets and only keys within
-//          beta = 2 D / w (+ float slack) of their shared edge; such "edge"
-//          elements are ranked across the adjacent buckets, all others inside
-//          their own bucket.  Elements beyond b*+1 cannot reach rank k;
-//          out-of-radius elements can only sit in the top bucket.
-// A set G beyond its capacity (or a key bound too loose for the bucket width)
-// falls back to the reference's serial insertion -- exact by construction.
+//  keys    every candidate gets a cheap float key a ~ d^2 with a proven
+//          absolute error bound D (|a - d^2| <= D);
+//  roads   a 128-bucket histogram of a over [0, rho^2] (rho: a hint-narrowed
+//          radius that provably covers the k nearest, or the full disc)
+//          gives the threshold bucket b*; the candidates of buckets <= b*+1
+//          are counting-sort scattered into a small set G (about k+1
+//          entries), sorted by odd-even transposition rounds (G is already
+//          block-sorted by bucket), and each sorted position is the
+//          reference's rank unless a neighbour lies within 2D of it (a near
+//          tie) or its key may lie beyond the radius; only those get the
+//          glibc-exact FP64 hypot (ds_math.cuh) and an exact (d, id) rank
+//          inside their near-tie cluster.  Elements beyond b*+1 cannot reach
+//          rank k;
+//  partners at most 32 candidates, ranked by counting key compares over the
+//          warp, the same neighbour checks.
+// A set the fast paths cannot rank (G beyond its capacity, a key bound too
+// loose for the bucket width, more than 32 partners, a near tie among the
+// partners) falls back to the reference's serial insertion -- exact by
+// construction.  Rows are staged in shared memory and leave by TMA bulk
+// stores.
 #include "ds_internal.cuh"
 #include "ds_obs_out.cuh"
 #include "ds_rows.cuh"
