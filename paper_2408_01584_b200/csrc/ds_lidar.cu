@@ -2,13 +2,13 @@
 // observation.py:223-280; _ray_angles 213-220; raycast_obbs_arr
 // geometry.py:399-424; raycast_segments_arr 380-396).
 //
-// One CTA per world, one warp per controlled agent, each lane owns rays
-// lane, lane+32, ...  Per ray:
-//  * boxes: every visible partner within max_range + circumradius (the
-//    reference's candidate set) is first rejected cheaply when the ray's line
-//    passes farther than its circumradius (+1 mm) from its centre or it lies
-//    behind the origin -- a superset test -- then the exact FP64 slab test
-//    of raycast_obbs_arr gives the distance; the minimum is the agent hit;
+// One CTA per world, one warp per controlled agent (rows handed to warps
+// dynamically), each lane owns rays lane, lane+32, ...  Per ray:
+//  * boxes, box-major: the visible partners within max_range +
+//    circumradius (the reference's candidate set, compacted first) are
+//    tested with the exact FP64 slab test of raycast_obbs_arr only against
+//    the rays inside a conservative angular interval around their bounding
+//    circle; the minimum is the agent hit;
 //  * road segments, segment-major: the warp visits the grid cells of the
 //    max-range disc ring by ring around the origin's cell, skips cells whose
 //    rays all hit something nearer already, and strides its lanes over the

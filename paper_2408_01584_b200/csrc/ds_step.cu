@@ -8,10 +8,13 @@
 //   B  SAT agent-agent and slab agent-road-edge collisions   (engine.py:420-459)
 //   C  goal reward, removal, collision behaviour, horizon    (engine.py:461-492)
 //   D  outputs, episode record, optional VecDriveEnv auto-reset
-// State is FP64 in HBM (SURVEY.md §7 "hard parts"); the broad phase is exact
-// brute force over the world's agents held in shared memory and over the road
-// edges binned in the world's uniform grid (the reference's BVH only prunes:
-// its results are pinned equal to brute force, tests/test_acceptance.py:193-219).
+// State is FP64 in HBM (SURVEY.md §7 "hard parts").  The broad phases only
+// prune, the exact FP64 narrow phases decide (the reference's BVH likewise
+// only prunes: its results are pinned equal to brute force,
+// tests/test_acceptance.py:193-219): agent pairs by sweep and prune over a
+// counting sort of x-bins with a float circumcircle test, road edges by the
+// world's uniform grid with float AABB and separating-axis filters whose
+// margins bound their rounding.
 #include "ds_internal.cuh"
 
 namespace ds {
