@@ -45,6 +45,18 @@ __device__ unsigned long long g_obs_stats[8];
 #define OBS_STAT(i, v) \
   do { } while (0)
 #endif
+// Dev-only CTA timeline (a build with -DDS_OBS_TIMES; tools/obs_times.py):
+// per world [sm, start, prologue end, end of warp 0..31's row loop, thread 0
+// staged, after the prologue barrier]
+#ifdef DS_OBS_TIMES
+constexpr int kTimesW = 37;
+__device__ unsigned long long g_obs_times[8192 * kTimesW];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNB = 128;       // histogram buckets
@@ -895,6 +907,14 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     const float *scale, int32_t *sel_idx, int obs_width) {
   const int w = blockIdx.x;
   if (mask && !mask[w]) return;
+#ifdef DS_OBS_TIMES
+  if (threadIdx.x == 0 && w < 8192) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_obs_times[w * kTimesW] = sm;
+    g_obs_times[w * kTimesW + 1] = gtimer();
+  }
+#endif
   // every per-world offset in one round of independent loads
   const int64_t c0 = T.c_off[w], c1 = T.c_off[w + 1];
   const int64_t a0 = T.a_off[w], a1 = T.a_off[w + 1];
@@ -978,6 +998,8 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   // a second group of threads -- the road-selection parameters and partner
   // key positions: one thread per (agent, part), overlapping the points'
   // bulk copy (the two parts split the prologue's critical path)
+  // row -> agent loads issued first: in flight across the staging below
+  const int ra_pre = (int)threadIdx.x < nrow ? T.row_agent[c0 + threadIdx.x] : 0;
   float e_own = 0.0f;
   for (int u = threadIdx.x; u < 2 * A; u += blockDim.x) {
     const bool tabs = u < A;
@@ -1043,9 +1065,20 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   if (lane == 0) e_max_w[warp] = e_own;
   for (int i = A + (int)threadIdx.x; i < pad32(A); i += blockDim.x) AT.pxy[i] = make_float2(1e30f, 1e30f);
   // row -> local agent, so the row loop starts from shared memory
-  for (int r = threadIdx.x; r < nrow; r += blockDim.x) AT.rloc[r] = (uint16_t)(T.row_agent[c0 + r] - a0);
+  if ((int)threadIdx.x < nrow) AT.rloc[threadIdx.x] = (uint16_t)(ra_pre - a0);
+  for (int r = threadIdx.x + blockDim.x; r < nrow; r += blockDim.x)
+    AT.rloc[r] = (uint16_t)(T.row_agent[c0 + r] - a0);
+#ifdef DS_OBS_TIMES
+  if (threadIdx.x == 0 && w < 8192) g_obs_times[w * kTimesW + 35] = gtimer();
+#endif
   __syncthreads();
+#ifdef DS_OBS_TIMES
+  if (threadIdx.x == 0 && w < 8192) g_obs_times[w * kTimesW + 36] = gtimer();
+#endif
   if (SharedPts) mbar_wait(&pts_bar, 0);
+#ifdef DS_OBS_TIMES
+  if (threadIdx.x == 0 && w < 8192) g_obs_times[w * kTimesW + 2] = gtimer();
+#endif
   const double *ax = AT.x, *ay = AT.y, *ah = AT.h, *av = AT.v, *ac = AT.c, *as = AT.s;
   const float *al = AT.l, *aw = AT.w;
   // the partners' selection parameters (per world): E = both positions'
@@ -1234,6 +1267,9 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     }
   }
   if (bulk_out && lane == 0) bulk_row_wait();   // the staging must outlive the copies
+#ifdef DS_OBS_TIMES
+  if (lane == 0 && w < 8192) g_obs_times[w * kTimesW + 3 + warp] = gtimer();
+#endif
 }
 
 #ifdef DS_OBS_STATS
@@ -1243,6 +1279,13 @@ extern "C" int ds_debug_obs_stats(unsigned long long *out) {
   unsigned long long z[8] = {0};
   cudaMemcpyToSymbol(ds::g_obs_stats, z, sizeof(z));
   return 0;
+}
+namespace ds {
+#endif
+#ifdef DS_OBS_TIMES
+}  // namespace ds
+extern "C" int ds_debug_obs_times(unsigned long long *out) {
+  return (int)cudaMemcpyFromSymbol(out, ds::g_obs_times, sizeof(ds::g_obs_times));
 }
 namespace ds {
 #endif
