@@ -340,7 +340,7 @@ struct RoadSrcShared {
     geo->range((float)rho, lane, b, c);
     rows.build(b - p0, c, lane, fscr);
   }
-  // cover() from the raw cell-table values of GeoRow::range_issue
+  // cover() from the raw cell-table values of RowGeo::range_issue_async
   __device__ __forceinline__ void cover_raw(int v0, int v1, int lane) {
     rows.build(v0 - p0, v1 - v0, lane, fscr);
   }
@@ -693,19 +693,26 @@ __device__ __forceinline__ int select_direct(const Src &src, int k, const SelPar
   bound_out = 0.0f;
   if (n == 0) return 0;
   if (n > 32) return -1;
+  if (lane >= n && lane < ((n + 3) & ~3)) S.ga()[lane] = INFINITY;   // whole float4s below
   __syncwarp();
   // one candidate per lane, ranked by counting (key, payload) order over the
   // n broadcast keys; keys more than 2D apart order exactly like the
   // distances.  (key, payload) order = (key bits, lane): G was compacted in
-  // visit order, so payloads ascend with the lane.  One 32-bit shuffle per
-  // broadcast key (non-negative floats order like their bit patterns); equal
-  // keys are ranked by lane with one match.
+  // visit order, so payloads ascend with the lane.  The keys are read back
+  // by broadcast shared loads, four per load; equal keys are ranked by lane
+  // with one match.
   const float a = lane < n ? S.ga()[lane] : INFINITY;
   const int pl = lane < n ? S.gpl()[lane] : 0x7fffffff;
   const unsigned ab = __float_as_uint(a);
   int rank = __popc(__match_any_sync(kFull, ab) & ((1u << lane) - 1u));
-#pragma unroll 4
-  for (int j = 0; j < n; ++j) rank += __shfl_sync(kFull, ab, j) < ab ? 1 : 0;
+  // the n keys read back four at a time by broadcast shared loads (padded
+  // with +inf, which never counts)
+  const float4 *g4 = reinterpret_cast<const float4 *>(S.ga());
+#pragma unroll 2
+  for (int j = 0; j < n; j += 4) {
+    const float4 q = g4[j >> 2];
+    rank += (q.x < a ? 1 : 0) + (q.y < a ? 1 : 0) + (q.z < a ? 1 : 0) + (q.w < a ? 1 : 0);
+  }
   // near ties between sorted neighbours, staged in the idle pass-1 buffer
   float *const srt = S.ca();
   if (lane < n) srt[rank] = a;
@@ -1083,8 +1090,11 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   const float *al = AT.l, *aw = AT.w;
   // the partners' selection parameters (per world): E = both positions'
   // float rounding + the float subtraction
-  SelParams PP;
+  // (kept in shared memory -- one copy per warp -- and read where used
+  // instead of in registers held across the row loop)
+  __shared__ SelParams PP_w[WARPS];
   {
+    SelParams PP;
     float em = lane < WARPS ? e_max_w[lane] : 0.0f;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) em = fmaxf(em, __shfl_xor_sync(kFull, em, off));
@@ -1097,7 +1107,10 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     PP.rho = radius;
     PP.restricted = false;
     PP.serial = !(PP.R.beta < 0.125f);
+    if (lane == 0) PP_w[warp] = PP;
+    __syncwarp();
   }
+  const SelParams &PP = PP_w[warp];
 
   // float32 rows without normalisation leave by bulk stores
   const bool bulk_out = O.dtype == DS_OBS_F32 && scale == nullptr;
@@ -1143,8 +1156,10 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     P.serial = pd.z & 2;
     const RowGeo geo{T.pt_cell_start + cbase, pa.x, pa.y, (float)cs, (float)inv_cs, pa.z, nx, ny, pd.x, pd.y};
     // the road rows' cell-table loads stay in flight across the partners
-    int rv0 = 0, rv1 = 0;
-    if (SharedPts && cap_r > 0) geo.range_issue((float)(P.restricted ? P.rho : reach), lane, rv0, rv1);
+    // (into the histogram words, unused until the road selection; no
+    // registers are held across the partners)
+    int *const cellv = reinterpret_cast<int *>(wb + WL.hc);
+    if (SharedPts && cap_r > 0) geo.range_issue_async((float)(P.restricted ? P.rho : reach), lane, cellv);
 
     // ---- partners: the picks are kept aside (psel); their slots are formed
     // while the selected road records are in flight
@@ -1163,7 +1178,9 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
       if (SharedPts) {
         RoadSrcShared rsrc{pts, static_cast<const ds_point_rec *>(T.gpt_rec), (int)p0, pa.x, pa.y, px,
                            py, &geo, reinterpret_cast<int *>(wb + WL.fr)};
-        rsrc.cover_raw(rv0, rv1, lane);
+        cp_async_wait_all();
+        __syncwarp();
+        rsrc.cover_raw(cellv[lane], cellv[32 + lane], lane);
         mr = select_topk<false, kEPL>(rsrc, cap_r, radius, P, S, lane, bound);
       } else {
         RoadSrcGlobal rsrc{T.gpt_x, T.gpt_y, T.gpt_id, (int)p0, np, px, py, &geo,
@@ -1173,8 +1190,10 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
       }
     }
     if (St.obs_hint && lane == 0)
+      // (pa.x, pa.y) = (float)(px - gx0), (float)(py - gy0), re-read from
+      // the staged tables instead of holding the grid origin across the row
       reinterpret_cast<float4 *>(St.obs_hint)[g] =
-          make_float4(bound, (float)(px - gx0), (float)(py - gy0), 0.0f);
+          make_float4(bound, AT.pa[i].x, AT.pa[i].y, 0.0f);
     // the selected records (32 B, one sector each) are fetched into the dead
     // selection scratch at the END of the road block ([road_end - 32 cap_r,
     // road_end)): the slots of batch u (44 B each, written from the start)

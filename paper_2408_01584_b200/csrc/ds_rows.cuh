@@ -42,27 +42,41 @@ struct RowGeo {
       nrows = nrows < 32 ? nrows : 32;
     }
   }
-  // range() split in two: issue the lane's two cell-table loads (raw
-  // values, so they can stay in flight across unrelated work) ...
-  __device__ __forceinline__ void range_issue(float reach, int lane, int &v0, int &v1) const {
-    v0 = v1 = 0;
-    if (lane >= nrows) return;
-    const int iy = iy0 + lane;
-    const float ylo = (float)iy * cs, yhi = ylo + cs;
-    float dyb = 0.0f;
-    if (py < ylo) dyb = ylo - py;
-    else if (py > yhi) dyb = py - yhi;
-    const float r = reach + marg;
-    if (dyb > r) return;
-    const float half = sqrtf(r * r - dyb * dyb) + marg;
-    const float fx0 = (px - half) * inv_cs, fx1 = (px + half) * inv_cs;
-    if (fx1 < 0.0f || fx0 >= (float)nx) return;
-    const int ix0 = clampf(floorf(fx0), 0, nx - 1), ix1 = clampf(floorf(fx1), 0, nx - 1);
-    const int *c = cell_start + (int64_t)iy * nx;
-    v0 = c[ix0];
-    v1 = c[ix1 + 1];
+  // range() split in two: the lane's two cell-table entries copied
+  // asynchronously (cp.async, 4 B each) into shared dst[lane] /
+  // dst[32 + lane] (zeros for a lane without cells), so nothing is held in
+  // registers while they are in flight across unrelated work.  The caller
+  // waits (cp.async.wait_all) and syncs the warp.
+  __device__ __forceinline__ void range_issue_async(float reach, int lane, int *dst) const {
+    const int *s0 = nullptr, *s1 = nullptr;
+    if (lane < nrows) {
+      const int iy = iy0 + lane;
+      const float ylo = (float)iy * cs, yhi = ylo + cs;
+      float dyb = 0.0f;
+      if (py < ylo) dyb = ylo - py;
+      else if (py > yhi) dyb = py - yhi;
+      const float r = reach + marg;
+      if (dyb <= r) {
+        const float half = sqrtf(r * r - dyb * dyb) + marg;
+        const float fx0 = (px - half) * inv_cs, fx1 = (px + half) * inv_cs;
+        if (!(fx1 < 0.0f || fx0 >= (float)nx)) {
+          const int ix0 = clampf(floorf(fx0), 0, nx - 1), ix1 = clampf(floorf(fx1), 0, nx - 1);
+          const int *c = cell_start + (int64_t)iy * nx;
+          s0 = c + ix0;
+          s1 = c + ix1 + 1;
+        }
+      }
+    }
+    if (s0) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + lane)),
+                   "l"(s0) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + 32 + lane)),
+                   "l"(s1) : "memory");
+    } else {
+      dst[lane] = 0;
+      dst[32 + lane] = 0;
+    }
   }
-  // ... and the (start, count) they encode (start = v0, count = v1 - v0)
   // range of lane's row for radius `reach` (a superset of the disc's points)
   __device__ __forceinline__ void range(float reach, int lane, int &sb, int &cnt) const {
     sb = 0;
