@@ -933,7 +933,8 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t pts_bar;
   __shared__ float e_max_w[WARPS];   // per warp: largest float rounding of an agent position
-  __shared__ int next_row;           // rows are handed out dynamically (no tail imbalance)
+  __shared__ int next_row;
+  __shared__ float bound_w[WARPS];   // per warp: the road selection's k-th distance bound           // rows are handed out dynamically (no tail imbalance)
   constexpr bool kFixed = CAPA > 0;
   // G positions per lane in the sort (even; runtime caps <= kSelCap: 6)
   constexpr int kEPL = kFixed ? ((gcap_of(CAPA, CAPR) + 63) / 64) * 2 : 2 * ((kSelCap + 48 + 63) / 64);
@@ -944,7 +945,7 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   // shared memory: [per-warp scratch x WARPS][road points][agent tables] --
   // the scratch and the points sit at (compile-time) constant offsets
   // lane / warp from opaque moves: the compiler keeps them in registers
-  // instead of re-reading the special registers (S2R) under register pressure
+  // instead of re-reading the special registers (S2R)
   int lane, warp;
   asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
   warp = __shfl_sync(kFull, (int)threadIdx.x >> 5, 0);
@@ -1122,7 +1123,6 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   for (int r = warp; r < nrow; r = grab_row()) {
     const int64_t orow = c0 + r;
     const int i = AT.rloc[r];
-    const int64_t g = a0 + i;
     const uint16_t f = AT.flg[i];
     if (f & (DS_F_DONE | DS_F_REMOVED)) {
       // finished / removed rows are zero-filled (engine.py:502-512)
@@ -1141,8 +1141,7 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     // the staged row copies the output row's 16-B phase (vector write-out)
     const int out_phase = out_row_phase(O, orow);
     float *const row = row0 - ((row0_phase - out_phase) & 3);   // contiguous staged row
-    const double px = ax[i], py = ay[i], h = ah[i];
-    const double ch = ac[i], sh = as[i];
+    const double px = ax[i], py = ay[i];
     const float4 pa = AT.pa[i], pb = AT.pb[i];
     const double2 pc = AT.pc[i];
     const int4 pd = AT.pd[i];
@@ -1173,7 +1172,10 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
 
     // ---- road points: lane l owns cell row iy0 + l of the disc
     int mr = 0;
-    float bound = 0.0f;
+    // the k-th distance bound goes to shared memory (one word per warp): it
+    // is produced before the ranking and consumed after it
+    float &bound = bound_w[warp];
+    if (lane == 0) bound = 0.0f;
     if (cap_r > 0) {
       if (SharedPts) {
         RoadSrcShared rsrc{pts, static_cast<const ds_point_rec *>(T.gpt_rec), (int)p0, pa.x, pa.y, px,
@@ -1189,11 +1191,14 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
         mr = select_topk<false, kEPL>(rsrc, cap_r, radius, P, S, lane, bound);
       }
     }
+    // the agent's index, heading and rotation re-read from the staged tables
+    // after the selections (instead of held in registers across them)
+    const int ii = AT.rloc[r];
+    const double h = ah[ii], ch = ac[ii], sh = as[ii];
     if (St.obs_hint && lane == 0)
-      // (pa.x, pa.y) = (float)(px - gx0), (float)(py - gy0), re-read from
-      // the staged tables instead of holding the grid origin across the row
-      reinterpret_cast<float4 *>(St.obs_hint)[g] =
-          make_float4(bound, AT.pa[i].x, AT.pa[i].y, 0.0f);
+      // (pa.x, pa.y) = (float)(px - gx0), (float)(py - gy0)
+      reinterpret_cast<float4 *>(St.obs_hint)[a0 + ii] =
+          make_float4(bound, AT.pa[ii].x, AT.pa[ii].y, 0.0f);
     // the selected records (32 B, one sector each) are fetched into the dead
     // selection scratch at the END of the road block ([road_end - 32 cap_r,
     // road_end)): the slots of batch u (44 B each, written from the start)
@@ -1220,7 +1225,7 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
       slot[0] = (float)(dx * ch + dy * sh);
       slot[1] = (float)(dy * ch - dx * sh);
       slot[2] = (float)wrap(ah[j] - h);
-      slot[3] = (float)(av[j] - av[i]);
+      slot[3] = (float)(av[j] - av[ii]);
       slot[4] = (float)al[j];
       slot[5] = (float)aw[j];
       slot[6] = 1.0f;
