@@ -130,8 +130,11 @@ __device__ __forceinline__ int cell_of(double v, int lo, int hi) {
 }
 
 // Any road-edge segment of world w touching box (cx, cy, ck, sk, hl, hw)?
-__device__ bool offroad_query(const ds_tables &T, const ds_config &C, int w, double cx,
-                              double cy, double ck, double sk, double hl, double hw) {
+// The box's FP64 values are read from the shared tables (sh, agent i): the
+// float filter loop holds only floats, the exact phase re-reads the rest.
+__device__ bool offroad_query(const ds_tables &T, const ds_config &C, int w, const StepShared &sh,
+                              int i) {
+  const double cx = sh.x[i], cy = sh.y[i], ck = sh.c[i], sk = sh.s[i], hl = sh.hl[i], hw = sh.hw[i];
   const int nx = T.grid_nx[w], ny = T.grid_ny[w];
   const double x0 = T.grid_x0[w], y0 = T.grid_y0[w], cs = C.grid_cell;
   const int64_t cbase = T.grid_cell_off[w];
@@ -194,11 +197,18 @@ __device__ bool offroad_query(const ds_tables &T, const ds_config &C, int w, dou
         const double2 *er = reinterpret_cast<const double2 *>(T.eseg_rec) + 2 * (int64_t)(k0 + v);
         const double2 e0 = er[0], e1 = er[1];
         const double ax = e0.x, ay = e0.y, bx = e1.x, by = e1.y;
+        // the box from shared memory again (the same values as above; the
+        // empty asm keeps the compiler from holding the first reads live)
+        asm volatile("" ::: "memory");
+        const double qx = sh.x[i], qy = sh.y[i], qk = sh.c[i], qs = sh.s[i];
+        const double ql = sh.hl[i], qw = sh.hw[i];
+        const double qrx = ql * fabs(qk) + qw * fabs(qs) + 0.011;
+        const double qry = ql * fabs(qs) + qw * fabs(qk) + 0.011;
         // segment AABB vs box AABB (with slack): a superset prefilter
-        if (fmax(ax, bx) < cx - rx || fmin(ax, bx) > cx + rx || fmax(ay, by) < cy - ry ||
-            fmin(ay, by) > cy + ry)
+        if (fmax(ax, bx) < qx - qrx || fmin(ax, bx) > qx + qrx || fmax(ay, by) < qy - qry ||
+            fmin(ay, by) > qy + qry)
           continue;
-        if (seg_box_hit(cx, cy, ck, sk, hl, hw, ax, ay, bx, by)) return true;
+        if (seg_box_hit(qx, qy, qk, qs, ql, qw, ax, ay, bx, by)) return true;
       }
     }
   }
@@ -464,8 +474,7 @@ __global__ void __launch_bounds__(MAXT, MINB) step_kernel(ds_tables T, ds_config
   if (act_here && sh.elig[tid]) {
     collided = sh.hit[tid] != 0;
     if (!(sf & DS_SF_PEDESTRIAN))
-      offroad = offroad_query(T, C, w, sh.x[tid], sh.y[tid], sh.c[tid], sh.s[tid], sh.hl[tid],
-                              sh.hw[tid]);
+      offroad = offroad_query(T, C, w, sh, tid);
   }
   if (collided) f |= DS_F_COLLIDED;
   if (offroad) f |= DS_F_OFFROAD;
