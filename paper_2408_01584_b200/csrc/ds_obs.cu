@@ -51,6 +51,7 @@ __device__ unsigned long long g_obs_stats[8];
 #ifdef DS_OBS_TIMES
 constexpr int kTimesW = 37;
 __device__ unsigned long long g_obs_times[8192 * kTimesW];
+__device__ unsigned int g_row_dur[8192 * 128];   // per (world, row < 128): row time (ns)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1120,7 +1121,19 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
     if (lane == 0) v = atomicAdd(&next_row, 1);
     return __shfl_sync(kFull, v, 0);
   };
+#ifdef DS_OBS_TIMES
+  int prev_r = -1;
+  unsigned long long t_prev = 0;
+#endif
   for (int r = warp; r < nrow; r = grab_row()) {
+#ifdef DS_OBS_TIMES
+    {
+      const unsigned long long t_now = gtimer();
+      if (lane == 0 && prev_r >= 0 && prev_r < 128 && w < 8192) g_row_dur[w * 128 + prev_r] = (unsigned)(t_now - t_prev);
+      prev_r = r;
+      t_prev = t_now;
+    }
+#endif
     const int64_t orow = c0 + r;
     const int i = AT.rloc[r];
     const uint16_t f = AT.flg[i];
@@ -1292,7 +1305,11 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   }
   if (bulk_out && lane == 0) bulk_row_wait();   // the staging must outlive the copies
 #ifdef DS_OBS_TIMES
-  if (lane == 0 && w < 8192) g_obs_times[w * kTimesW + 3 + warp] = gtimer();
+  {
+    const unsigned long long t_now = gtimer();
+    if (lane == 0 && prev_r >= 0 && prev_r < 128 && w < 8192) g_row_dur[w * 128 + prev_r] = (unsigned)(t_now - t_prev);
+    if (lane == 0 && w < 8192) g_obs_times[w * kTimesW + 3 + warp] = t_now;
+  }
 #endif
 }
 
@@ -1310,6 +1327,9 @@ namespace ds {
 }  // namespace ds
 extern "C" int ds_debug_obs_times(unsigned long long *out) {
   return (int)cudaMemcpyFromSymbol(out, ds::g_obs_times, sizeof(ds::g_obs_times));
+}
+extern "C" int ds_debug_obs_row_dur(unsigned int *out) {
+  return (int)cudaMemcpyFromSymbol(out, ds::g_row_dur, sizeof(ds::g_row_dur));
 }
 namespace ds {
 #endif

@@ -40,3 +40,32 @@ for k, v in [("prologue", 32 * pro.sum()), ("row loop", loop.sum()), ("CTA tail"
     print(f"  {k:28s} {100 * v / slots:5.1f} % of warp-slot time")
 last = np.sort(tend - base)
 print("last CTA ends at", last[-1] / 1e3, "us; 95% of CTAs done by", last[int(0.95 * nw)] / 1e3, "us")
+
+# Row durations of two consecutive steps: does the previous step's duration
+# predict this one's, and what would handing rows out longest-first save?
+def row_durs():
+    buf = (ctypes.c_uint * (8192 * 128))()
+    N.lib().ds_debug_obs_row_dur(buf)
+    return np.frombuffer(buf, dtype=np.uint32).reshape(8192, 128)[:nw].astype(np.float64)
+d1 = row_durs()
+b.step(random_actions(b.n_controlled, cfg, 0, 99, "cuda:0"), auto_reset=True)
+torch.cuda.synchronize()
+d2 = row_durs()
+print("row time mean %.2f us, cv %.2f, max/mean %.2f" % (d2.mean() / 1e3, d2.std() / d2.mean(), d2.max() / d2.mean()))
+print("corr(prev step, this step) per row: %.3f" % np.corrcoef(d1.ravel(), d2.ravel())[0, 1])
+import heapq
+def makespan(d, order, nwarp=32):
+    fin = [0.0] * nwarp
+    h = [(0.0, k) for k in range(nwarp)]
+    for r in order:
+        t, k = heapq.heappop(h)
+        heapq.heappush(h, (t + d[r], k))
+    return max(t for t, _ in h), sum(d) / nwarp
+res = {"index": [], "lpt_prev": [], "lpt_oracle": []}
+for wi in range(0, nw, 8):
+    d = d2[wi]
+    for name, order in [("index", range(128)), ("lpt_prev", np.argsort(-d1[wi], kind="stable")),
+                        ("lpt_oracle", np.argsort(-d, kind="stable"))]:
+        m, ideal = makespan(d, order)
+        res[name].append(m / ideal)
+print({k: round(float(np.mean(v)), 4) for k, v in res.items()}, "(makespan / ideal, simulated)")
