@@ -331,10 +331,17 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
     e[5] = (float)hypot(gx, gy);
     e[6] = (f & DS_F_COLLIDED) ? 1.0f : 0.0f;
   }
+  // the grid origin in shared memory, read once per row where used (not
+  // held in registers across the row loop)
+  __shared__ double g_org[2];
+  if (threadIdx.x == 0) {
+    g_org[0] = T.grid_x0[w];
+    g_org[1] = T.grid_y0[w];
+  }
   __syncthreads();
 
   const int64_t cbase = T.grid_cell_off[w];
-  const double gx0 = T.grid_x0[w], gy0 = T.grid_y0[w], cs = C.grid_cell;
+  const double cs = C.grid_cell;
   const int gnx = T.grid_nx[w], gny = T.grid_ny[w];
   const double max_range = C.max_range;
   const bool full_circle = FULL || C.obs_mode == DS_OBS_LIDAR || C.fov >= kTwoPi;
@@ -457,6 +464,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
     // cells are flattened into full warp batches, and their (segment, ray)
     // pairs again (the segment batch is staged per warp in shared memory)
     {
+      asm volatile("" ::: "memory");
+      const double gx0 = g_org[0], gy0 = g_org[1];
       const double inv_cs = 1.0 / cs;
       const int ocx = (int)fmin(fmax(floor((ox - gx0) * inv_cs), -1e6), 1e6);
       const int ocy = (int)fmin(fmax(floor((oy - gy0) * inv_cs), -1e6), 1e6);
