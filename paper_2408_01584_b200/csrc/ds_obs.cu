@@ -1006,15 +1006,24 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   // agent tables and the ego block of every agent (fp:228-238), then -- by
   // a second group of threads -- the road-selection parameters and partner
   // key positions: one thread per (agent, part), overlapping the points'
-  // bulk copy (the two parts split the prologue's critical path)
+  // bulk copy (the parts split the prologue's critical path)
   // row -> agent loads issued first: in flight across the staging below
   const int ra_pre = (int)threadIdx.x < nrow ? T.row_agent[c0 + threadIdx.x] : 0;
   float e_own = 0.0f;
-  for (int u = threadIdx.x; u < 2 * A; u += blockDim.x) {
-    const bool tabs = u < A;
-    const int i = tabs ? u : u - A;
+  // three parts per agent, one thread each: the tables and the rotation,
+  // the goal distance (an FP64 hypot, independent of the rotation), the
+  // road-selection parameters
+  for (int u = threadIdx.x; u < 3 * A; u += blockDim.x) {
+    const int part = u < A ? 0 : (u < 2 * A ? 1 : 2);
+    const bool tabs = part == 0;
+    const int i = u - part * A;
     const int64_t g = a0 + i;
     const double px = St.x[g], py = St.y[g];
+    if (part == 1) {
+      const double gx = T.goal_x[g] - px, gy = T.goal_y[g] - py;
+      AT.ego[8 * i + 5] = (float)hypot(gx, gy);
+      continue;
+    }
     const uint16_t f = St.flags[g];
     if (tabs) {
       const double hd = St.heading[g], v = St.speed[g];
@@ -1031,7 +1040,6 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
       e[2] = (float)wd;
       e[3] = (float)(gx * ch + gy * sh);
       e[4] = (float)(gy * ch - gx * sh);
-      e[5] = (float)hypot(gx, gy);
       e[6] = (f & DS_F_COLLIDED) ? 1.0f : 0.0f;
       continue;
     }
