@@ -6,6 +6,8 @@
 
 #include <new>
 
+#include <vector>
+
 #include "ds_internal.cuh"
 
 namespace {
@@ -81,6 +83,24 @@ int ds_create(const ds_tables *tables, const ds_config *cfg, ds_state *state, in
   if (e != cudaSuccess) {
     delete h;
     return cuda_fail(e, "cudaDeviceGetAttribute");
+  }
+  // uniform per-world strides (one host read of the offsets at creation)
+  {
+    const int W = tables->n_worlds;
+    const int64_t *offs[3] = {tables->a_off, tables->c_off, tables->p_off};
+    int64_t *uni[3] = {&h->uni_a, &h->uni_c, &h->uni_p};
+    std::vector<int64_t> hv((size_t)W + 1);
+    for (int k = 0; k < 3; ++k) {
+      *uni[k] = 0;
+      if (W <= 0 || !offs[k] ||
+          cudaMemcpy(hv.data(), offs[k], hv.size() * sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+        continue;
+      const int64_t st = hv[1] - hv[0];
+      bool ok = hv[0] == 0 && st > 0;
+      for (int w = 1; ok && w <= W; ++w) ok = hv[w] == (int64_t)w * st;
+      if (ok) *uni[k] = st;
+    }
+    cudaGetLastError();
   }
   int amax = tables->max_agents < 1 ? 1 : tables->max_agents;
   h->step_threads = ((amax + 31) / 32) * 32;

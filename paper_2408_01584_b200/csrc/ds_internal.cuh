@@ -21,6 +21,10 @@ struct ds_handle {
   int obs_dtype;        // DS_OBS_F32 / DS_OBS_BF16
   int obs_stride;       // elements per observation row (>= obs_width)
   uint32_t ring_read;   // host mirror of entries already drained
+  // per-world strides when every world has the same number of agents /
+  // rows / road points (offset[w] = w * stride; 0: ragged): the observation
+  // kernel then forms its offsets without a dependent load
+  int64_t uni_a, uni_c, uni_p;
 };
 
 namespace ds {

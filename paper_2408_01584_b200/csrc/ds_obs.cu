@@ -904,6 +904,7 @@ __device__ int select_topk(Src src, int k, double radius, const SelParams &P, co
 // keeping (or rematerialising) them in registers.
 struct RadialK {
   double radius, reach, r2, D_fp64, cs, inv_cs, key_e;
+  int64_t uni_a, uni_c, uni_p;   // uniform per-world strides (0: read the offsets)
 };
 
 // AMAX > 0: the agent tables' stride as a compile-time constant (worlds of
@@ -924,9 +925,10 @@ __global__ void __launch_bounds__(WARPS * 32, (!SharedPts || WARPS <= 16) ? 2 : 
   }
 #endif
   // every per-world offset in one round of independent loads
-  const int64_t c0 = T.c_off[w], c1 = T.c_off[w + 1];
-  const int64_t a0 = T.a_off[w], a1 = T.a_off[w + 1];
-  const int64_t p0 = T.p_off[w], p1 = T.p_off[w + 1];
+  // (uniform worlds: formed from the strides, no dependent load)
+  const int64_t c0 = K.uni_c ? w * K.uni_c : T.c_off[w], c1 = K.uni_c ? c0 + K.uni_c : T.c_off[w + 1];
+  const int64_t a0 = K.uni_a ? w * K.uni_a : T.a_off[w], a1 = K.uni_a ? a0 + K.uni_a : T.a_off[w + 1];
+  const int64_t p0 = K.uni_p ? w * K.uni_p : T.p_off[w], p1 = K.uni_p ? p0 + K.uni_p : T.p_off[w + 1];
   const int nrow = (int)(c1 - c0);
   if (nrow == 0) return;
   const int A = (int)(a1 - a0);
@@ -1454,6 +1456,9 @@ cudaError_t launch_observe(const ds_handle *h, const uint8_t *mask, void *obs,
   K.cs = h->cfg.grid_cell;
   K.inv_cs = 1.0 / K.cs;
   K.key_e = (K.radius + 1.0) * 1.2e-7;
+  K.uni_a = h->uni_a;
+  K.uni_c = h->uni_c;
+  K.uni_p = h->uni_p;
   const ObsLaunch L{h, K, mask, O, scale, sel_idx, W, fixed, s};
   if (!h->obs_shared_pts) launch_radial<kWarpsGlobal, false>(L);
   else if (h->obs_warps == kWarpsShared) launch_radial<kWarpsShared, true>(L);
