@@ -87,10 +87,10 @@ int ds_create(const ds_tables *tables, const ds_config *cfg, ds_state *state, in
   // uniform per-world strides (one host read of the offsets at creation)
   {
     const int W = tables->n_worlds;
-    const int64_t *offs[3] = {tables->a_off, tables->c_off, tables->p_off};
-    int64_t *uni[3] = {&h->uni_a, &h->uni_c, &h->uni_p};
+    const int64_t *offs[4] = {tables->a_off, tables->c_off, tables->p_off, tables->r_off};
+    int64_t *uni[4] = {&h->uni_a, &h->uni_c, &h->uni_p, &h->uni_r};
     std::vector<int64_t> hv((size_t)W + 1);
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < 4; ++k) {
       *uni[k] = 0;
       if (W <= 0 || !offs[k] ||
           cudaMemcpy(hv.data(), offs[k], hv.size() * sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess)

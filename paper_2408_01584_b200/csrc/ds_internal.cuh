@@ -24,10 +24,22 @@ struct ds_handle {
   // per-world strides when every world has the same number of agents /
   // rows / road points (offset[w] = w * stride; 0: ragged): the observation
   // kernel then forms its offsets without a dependent load
-  int64_t uni_a, uni_c, uni_p;
+  int64_t uni_a, uni_c, uni_p, uni_r;
 };
 
 namespace ds {
+
+// Uniform per-world strides of the CSR offsets (0: ragged, read the offsets);
+// see ds_handle::uni_*
+struct WorldStrides {
+  int64_t a, c, r;
+  __device__ __forceinline__ int64_t a0(const ds_tables &T, int w) const { return a ? w * a : T.a_off[w]; }
+  __device__ __forceinline__ int64_t a1(const ds_tables &T, int w) const { return a ? (w + 1) * a : T.a_off[w + 1]; }
+  __device__ __forceinline__ int64_t c0(const ds_tables &T, int w) const { return c ? w * c : T.c_off[w]; }
+  __device__ __forceinline__ int64_t c1(const ds_tables &T, int w) const { return c ? (w + 1) * c : T.c_off[w + 1]; }
+  __device__ __forceinline__ int64_t r0(const ds_tables &T, int w) const { return r ? w * r : T.r_off[w]; }
+};
+inline WorldStrides world_strides(const ds_handle *h) { return WorldStrides{h->uni_a, h->uni_c, h->uni_r}; }
 
 // Largest supported max_agents_obs / max_road_points_obs (selection set size).
 constexpr int kSelCap = 128;

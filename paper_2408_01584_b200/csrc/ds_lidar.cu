@@ -267,12 +267,12 @@ __device__ __forceinline__ double ray_box(double ox, double oy, double dx, doubl
 template <int WARPS, int NR, bool FULL, int AMAX>
 __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 : 1)) obs_lidar_kernel(
     ds_tables T, ds_config C, ds_state St, const uint8_t *mask, const ObsOut O, const float *scale,
-    int obs_width) {
+    int obs_width, const WorldStrides U) {
   const int R = NR > 0 ? NR : C.n_rays;
   const int w = blockIdx.x;
   if (mask && !mask[w]) return;
-  const int64_t c0 = T.c_off[w];
-  const int nrow = (int)(T.c_off[w + 1] - c0);
+  const int64_t c0 = U.c0(T, w);
+  const int nrow = (int)(U.c1(T, w) - c0);
   if (nrow == 0) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int next_row;
@@ -303,8 +303,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 8 ? 4 : (WARPS <= 16 ? 2 
                                                 al16l((size_t)R * sizeof(float)));
   const int row0_phase = (int)((reinterpret_cast<uintptr_t>(row0) >> 2) & 3);
 
-  const int64_t a0 = T.a_off[w];
-  const int A = (int)(T.a_off[w + 1] - a0);
+  const int64_t a0 = U.a0(T, w);
+  const int A = (int)(U.a1(T, w) - a0);
   float *sego = reinterpret_cast<float *>(smem_raw + al16l((size_t)amax * (7 * sizeof(double) + 1)));
   for (int i = threadIdx.x; i < A; i += blockDim.x) {
     const int64_t g = a0 + i;
@@ -665,10 +665,10 @@ cudaError_t launch_lidar(const ds_handle *h, const uint8_t *mask, void *obs, con
   if (lidar_fast(h->cfg, h->tab.max_agents))
     obs_lidar_kernel<kLidarWarps, 64, true, kLidarStride>
         <<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(h->tab, h->cfg, h->st, mask, O,
-                                                                 scale, h->obs_width);
+                                                                 scale, h->obs_width, world_strides(h));
   else
     obs_lidar_kernel<kLidarWarps, 0, false, 0><<<h->tab.n_worlds, kLidarWarps * 32, h->obs_smem, s>>>(
-        h->tab, h->cfg, h->st, mask, O, scale, h->obs_width);
+        h->tab, h->cfg, h->st, mask, O, scale, h->obs_width, world_strides(h));
   return cudaGetLastError();
 }
 

@@ -231,20 +231,20 @@ __device__ __forceinline__ void reset_agent(const ds_tables &T, const ds_state &
 // variant: up to 255 registers, no spills of the FP64 state)
 template <int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) step_kernel(ds_tables T, ds_config C, ds_state S,
-                                                    ds_step_args a) {
+                                                    ds_step_args a, const WorldStrides U) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int w = blockIdx.x;
   const int tid = threadIdx.x;
-  const int64_t a0 = T.a_off[w];
-  const int A = (int)(T.a_off[w + 1] - a0);
-  const int64_t r_w = T.r_off[w];
+  const int64_t a0 = U.a0(T, w);
+  const int A = (int)(U.a1(T, w) - a0);
+  const int64_t r_w = U.r0(T, w);
   const int Tw = T.num_steps[w];
   const bool act_here = tid < A;
   const int64_t g = a0 + tid;
   const uint8_t sf = act_here ? T.sflags[g] : 0;
   const bool ctrl = sf & DS_SF_CONTROLLED;
   const int row = (act_here && ctrl) ? T.ctrl_row[g] : -1;
-  const int n_rows = (int)(T.c_off[w + 1] - T.c_off[w]);
+  const int n_rows = (int)(U.c1(T, w) - U.c0(T, w));
 
   if (S.episode_over[w]) {
     // Early return of World.step (engine.py:370-373): zero rewards/info,
@@ -619,13 +619,13 @@ cudaError_t configure_step_kernels(int max_dynamic_smem) {
 cudaError_t launch_step(const ds_handle *h, const ds_step_args *a, cudaStream_t s) {
   if (h->step_threads <= 128)   // 8 CTAs (32 warps) per SM at <= 64 registers
     step_kernel<128, DS_STEP_MINB><<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg,
-                                                                              h->st, *a);
+                                                                              h->st, *a, world_strides(h));
   else if (h->step_threads <= 256)
     step_kernel<256, 1><<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg,
-                                                                              h->st, *a);
+                                                                              h->st, *a, world_strides(h));
   else
     step_kernel<1024, 1><<<h->tab.n_worlds, h->step_threads, h->step_smem, s>>>(h->tab, h->cfg,
-                                                                               h->st, *a);
+                                                                               h->st, *a, world_strides(h));
   return cudaGetLastError();
 }
 
