@@ -121,6 +121,11 @@ __device__ __forceinline__ bool seg_box_hit(double cx, double cy, double ck, dou
   return true;
 }
 
+// float prefilter loads in flight per pass of the off-road scan
+#ifndef DS_OFF_INFLIGHT
+#define DS_OFF_INFLIGHT 2
+#endif
+
 // Clamp a floating cell coordinate to [lo, hi] before converting.
 __device__ __forceinline__ int cell_of(double v, int lo, int hi) {
   double f = floor(v);
@@ -163,14 +168,14 @@ __device__ bool offroad_query(const ds_tables &T, const ds_config &C, int w, con
     // the cells ix0..ix1 of one grid row are consecutive bins: one range
     const int64_t crow = cbase + (int64_t)iy * nx;
     const int b = T.eseg_cell_start[crow + ix0], e = T.eseg_cell_start[crow + ix1 + 1];
-    for (int k0 = b; k0 < e; k0 += 4) {
+    for (int k0 = b; k0 < e; k0 += DS_OFF_INFLIGHT) {
       // four float prefilter loads in flight, then the tests
-      float4 q[4];
+      float4 q[DS_OFF_INFLIGHT];
 #pragma unroll
-      for (int v = 0; v < 4; ++v)
+      for (int v = 0; v < DS_OFF_INFLIGHT; ++v)
         q[v] = k0 + v < e ? erel[k0 + v] : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
+      for (int v = 0; v < DS_OFF_INFLIGHT; ++v) {
         if (fmaxf(q[v].x, q[v].z) < fcx - frx || fminf(q[v].x, q[v].z) > fcx + frx ||
             fmaxf(q[v].y, q[v].w) < fcy - fry || fminf(q[v].y, q[v].w) > fcy + fry)
           continue;
